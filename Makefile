@@ -1,0 +1,37 @@
+# Builds the B200-native library and the CPU checkers.
+#
+#   make            -> paper_2409_16997_b200/lib/libifa_b200.so (sm_100a) + oracle
+#   make ref        -> oracle/_ref/* (needs /root/reference; CPU checker only)
+#
+# Every CUDA source is compiled for exactly one target:
+#   -gencode arch=compute_100a,code=sm_100a
+# No fast-math: the kernels restate the reference's IEEE float expressions.
+NVCC ?= /usr/local/cuda/bin/nvcc
+PKG := paper_2409_16997_b200
+CSRC := $(PKG)/csrc
+LIB := $(PKG)/lib/libifa_b200.so
+SRCS := $(CSRC)/abi.cu $(CSRC)/attn.cu $(CSRC)/quant.cu
+HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/ifa_internal.h include/ifa_b200.h
+NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
+           -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+
+all: $(LIB) oracle
+
+$(LIB): $(SRCS) $(HDRS)
+	@mkdir -p $(PKG)/lib
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) -lcuda 2> $(PKG)/lib/ptxas.log || (cat $(PKG)/lib/ptxas.log; exit 1)
+
+oracle:
+	$(MAKE) -s -C oracle all
+
+ref:
+	$(MAKE) -s -C oracle ref refa
+
+sass: $(LIB)
+	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > $(PKG)/lib/sass.txt
+
+clean:
+	rm -rf $(PKG)/lib
+	$(MAKE) -s -C oracle clean
+
+.PHONY: all oracle ref sass clean

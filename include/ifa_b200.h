@@ -1,0 +1,106 @@
+/*
+ * ifa_b200.h -- C-ABI of the B200-native INT-FlashAttention hot path.
+ *
+ * Drop-in boundary for the reference's CPU path (/root/reference/proj):
+ *
+ *   ifa_quantize_per_row      replaces ifa::quantize_per_row
+ *                             (include/ifa/quant.hpp:30, src/quant.cpp:44-57)
+ *   ifa_quantize_per_tensor   replaces ifa::quantize_per_tensor applied per (b,h)
+ *                             slice (include/ifa/quant.hpp:33, src/quant.cpp:59-69,
+ *                             caller src/eval.cpp:101)
+ *   ifa_int_flash_fwd         replaces ifa::int_flash_attention
+ *                             (include/ifa/attention.hpp:85-87,
+ *                             src/attention.cpp:235-357), batched over slices
+ *   ifa_last_error            replaces the what() of the C++ exceptions the
+ *                             reference throws (std::invalid_argument /
+ *                             std::overflow_error)
+ *
+ * Layout (reference include/ifa/matrix.hpp:16-90): every
+ * matrix is row-major and contiguous.  A batch of (b,h) slices is
+ * [slices][n][d] with no padding.  Q/K per-row scales are [slices][n] f32,
+ * the V tensor-level scale is one f32 per slice ([slices]), O is f32
+ * [slices][n][d].  Codes are int8 in [-127, 127].
+ *
+ * All pointers are DEVICE pointers on the current CUDA device unless stated
+ * otherwise; `stream` is a cudaStream_t (NULL = legacy default stream).
+ * Calls are asynchronous on `stream` and reentrant per stream.  Return
+ * values: 0 on success, otherwise one of the IFA_E* codes below with a
+ * message retrievable through ifa_last_error() (thread-local).
+ */
+#ifndef IFA_B200_H
+#define IFA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IFA_OK 0
+#define IFA_EINVAL 22     /* std::invalid_argument in the reference       */
+#define IFA_EOVERFLOW 75  /* std::overflow_error (int32 depth guard)      */
+#define IFA_ENOTSUP 95    /* shape this build does not run on the GPU     */
+#define IFA_ECUDA 1000    /* CUDA runtime / driver error                  */
+
+/* ifa_int_flash_fwd flags */
+#define IFA_FLAG_SQRT_D 1u /* AttentionConfig::apply_sqrt_d_scaling (attention.hpp:25-27) */
+#define IFA_FLAG_CAUSAL 2u /* extension (not in the reference): row i sees keys j <= i   */
+
+/* Device-resident mirror of ifa::PCodeAudit (attention.hpp:75-80).  Before
+ * a call the struct must hold {127, 0, 1, 0, 0} (ifa_audit_init()); the
+ * kernel folds its observations into it. */
+typedef struct ifa_pcode_audit {
+    int32_t min_code;
+    int32_t max_code;
+    int32_t row_max_block_hits_127; /* bool */
+    int32_t reserved;
+    int64_t rows_audited;
+} ifa_pcode_audit;
+
+/* Largest reduction depth for which k*127*127 < 2^31 (gemm.hpp:22). */
+#define IFA_MAX_INT_GEMM_DEPTH 133144
+
+/* Per-token quantization: codes[r][c] = round(x[r][c] / scales[r]) with
+ * scales[r] = max|x[r][:]| / 127 (all-zero row -> scale 0, codes 0).
+ * nonfinite_index (device, optional): if non-NULL it must hold INT64_MAX
+ * before the call and receives the smallest flat index of a NaN/Inf input
+ * (the reference rejects such input, quant.cpp:14-22). */
+int ifa_quantize_per_row(const float* x, int64_t rows, int64_t cols, int8_t* codes,
+                         float* scales, int64_t* nonfinite_index, void* stream);
+
+/* Tensor-level quantization applied independently to each of `slices`
+ * matrices of rows x cols: one scale per slice (slice_scales[s]).
+ * workspace: device buffer of >= 4*slices bytes (scratch). */
+int ifa_quantize_per_tensor(const float* x, int64_t slices, int64_t rows, int64_t cols,
+                            int8_t* codes, float* slice_scales, void* workspace,
+                            int64_t* nonfinite_index, void* stream);
+
+/* Full-INT8 flash attention forward over `slices` independent (b,h) slices
+ * of n x d (self-attention: N_q = N_kv = n).
+ *   br: the reference's row-block size; results do not depend on it
+ *       (accepted and validated for drop-in fidelity).
+ *   bc: KV block size; honoured exactly (it changes results).
+ *   audit: optional device ifa_pcode_audit.
+ * sv values must be finite and >= 0 (validated by the host shims; the
+ * reference rejects them in QuantizedAttentionInputs::validate).
+ * Supported on the GPU: 1 <= d <= 128, n >= 1, bc >= 1.  d > 128 returns
+ * IFA_ENOTSUP. */
+int ifa_int_flash_fwd(const int8_t* q, const float* sq, const int8_t* k, const float* sk,
+                      const int8_t* v, const float* sv, float* o, int64_t slices, int64_t n,
+                      int64_t d, int64_t br, int64_t bc, uint32_t flags,
+                      ifa_pcode_audit* audit, void* stream);
+
+/* Writes {127, 0, 1, 0, 0} into a device ifa_pcode_audit (async on stream). */
+int ifa_audit_init(ifa_pcode_audit* audit, void* stream);
+
+/* Message of the last failing call on this host thread ("" if none). */
+const char* ifa_last_error(void);
+
+/* Build/version string, e.g. "ifa_b200 0.1 sm_100a". */
+const char* ifa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IFA_B200_H */

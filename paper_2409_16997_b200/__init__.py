@@ -1,0 +1,26 @@
+"""B200-native INT-FlashAttention forward (arXiv 2409.16997 hot path).
+
+Per-token INT8 quantization of Q/K, per-slice tensor-level INT8
+quantization of V, and the fused full-INT8 flash-attention forward, as
+hand-written sm_100a kernels (TMA + tcgen05.mma kind::i8 + TMEM) behind the
+C-ABI in include/ifa_b200.h.  See DESIGN.md.
+"""
+from .api import (  # noqa: F401
+    AttentionConfig,
+    BlockSpec,
+    PCodeAudit,
+    QuantizedAttentionInputs,
+    QuantizedRows,
+    QuantizedTensor,
+    int_flash_attention,
+    quantize_per_row,
+    quantize_per_tensor,
+    version,
+)
+from ._lib import NativeLibraryError  # noqa: F401
+
+__all__ = [
+    "AttentionConfig", "BlockSpec", "PCodeAudit", "QuantizedAttentionInputs",
+    "QuantizedRows", "QuantizedTensor", "int_flash_attention", "quantize_per_row",
+    "quantize_per_tensor", "version", "NativeLibraryError",
+]

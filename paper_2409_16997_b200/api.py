@@ -1,0 +1,238 @@
+"""Host-side mirror of the reference's operator interface for the hot path.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/ifa/{quant,gemm,attention}.hpp:
+
+=============================  ==============================================
+reference                      here
+=============================  ==============================================
+``QuantizedRows``              :class:`QuantizedRows` (quant.hpp:17-20)
+``QuantizedTensor``            :class:`QuantizedTensor` (quant.hpp:23-26)
+``quantize_per_row``           :func:`quantize_per_row` (quant.hpp:30)
+``quantize_per_tensor``        :func:`quantize_per_tensor` (quant.hpp:33),
+                               applied per (b,h) slice as eval.cpp:101 does
+``BlockSpec``                  :class:`BlockSpec` (gemm.hpp:14-19)
+``AttentionConfig``            :class:`AttentionConfig` (attention.hpp:23-31)
+``QuantizedAttentionInputs``   :class:`QuantizedAttentionInputs`
+                               (attention.hpp:63-70, attention.cpp:213-233)
+``PCodeAudit``                 :class:`PCodeAudit` (attention.hpp:75-80)
+``int_flash_attention``        :func:`int_flash_attention` (attention.hpp:85-87)
+=============================  ==============================================
+
+Tensors are ``torch`` CUDA tensors (PyTorch is only the device-memory and
+stream plumbing); all arithmetic runs in libifa_b200.so.  Matrices may carry
+leading batch dimensions: ``[..., n, d]`` is a batch of independent (b,h)
+slices.  Exceptions: ``ValueError`` where the reference throws
+``std::invalid_argument``, ``OverflowError`` for ``std::overflow_error``.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import torch
+
+from . import _lib
+
+K_QUANT_MAX = 127                      # quant.hpp:14
+K_MAX_INT_GEMM_DEPTH = (1 << 31) // (127 * 127)  # gemm.hpp:22 (133144)
+_INT64_MAX = (1 << 63) - 1
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _require_cuda(t: torch.Tensor, dtype: torch.dtype, what: str) -> None:
+    if not isinstance(t, torch.Tensor):
+        raise ValueError(f"{what}: expected a torch tensor")
+    if t.device.type != "cuda":
+        raise ValueError(f"{what}: tensor must live on a CUDA device (no CPU fallback)")
+    if t.dtype != dtype:
+        raise ValueError(f"{what}: expected dtype {dtype}, got {t.dtype}")
+
+
+@dataclass
+class QuantizedRows:
+    """Token-level quantization: one scale per row (quant.hpp:17-20)."""
+    values: torch.Tensor   # int8 [..., n, d]
+    scales: torch.Tensor   # f32  [..., n]
+
+
+@dataclass
+class QuantizedTensor:
+    """Tensor-level quantization: one scale per (b,h) slice (quant.hpp:23-26)."""
+    values: torch.Tensor   # int8 [..., n, d]
+    scale: torch.Tensor    # f32  [...]   (0-dim for a single matrix)
+
+
+@dataclass
+class BlockSpec:
+    """Tile sizes (gemm.hpp:14-19).  Br does not change results; Bc does."""
+    Br: int = 64
+    Bc: int = 64
+
+    def validate(self) -> None:
+        if self.Br < 1 or self.Bc < 1:           # gemm.cpp:16-20
+            raise ValueError("BlockSpec: Br and Bc must be >= 1")
+
+
+@dataclass
+class AttentionConfig:
+    """attention.hpp:23-31, plus the ``causal`` extension (not in the reference)."""
+    blocks: BlockSpec = field(default_factory=BlockSpec)
+    apply_sqrt_d_scaling: bool = False
+    causal: bool = False
+
+    def validate(self) -> None:
+        self.blocks.validate()
+
+
+@dataclass
+class PCodeAudit:
+    """attention.hpp:75-80."""
+    min_code: int = 127
+    max_code: int = 0
+    row_max_block_hits_127: bool = True
+    rows_audited: int = 0
+
+
+@dataclass
+class QuantizedAttentionInputs:
+    q: QuantizedRows
+    k: QuantizedRows
+    v: QuantizedTensor
+
+    def validate(self) -> None:
+        """attention.cpp:213-233 (the sV check reads the scales back to the host)."""
+        qv = self.q.values
+        if qv.dim() < 2 or qv.shape[-2] < 1 or qv.shape[-1] < 1:
+            raise ValueError("quantized attention inputs: empty q")
+        n, d = qv.shape[-2], qv.shape[-1]
+        for name, t in (("k", self.k.values), ("v", self.v.values)):
+            if tuple(t.shape) != tuple(qv.shape):
+                raise ValueError(
+                    f"quantized attention inputs: q, k, v must all be {n}x{d} "
+                    f"(got {name} {tuple(t.shape)})")
+        for name, s in (("q", self.q.scales), ("k", self.k.scales)):
+            if tuple(s.shape) != tuple(qv.shape[:-1]):
+                raise ValueError(
+                    f"quantized attention inputs: scale vectors must have length {n}")
+        sv = self.v.scale
+        if tuple(sv.shape) != tuple(qv.shape[:-2]):
+            raise ValueError("quantized attention inputs: one v scale per slice expected")
+        bad = ~(torch.isfinite(sv) & (sv >= 0))
+        if bool(bad.any()):
+            raise ValueError("quantized attention inputs: bad v scale")
+
+
+def quantize_per_row(x: torch.Tensor, *, check_finite: bool = True,
+                     stream: Optional[torch.cuda.Stream] = None) -> QuantizedRows:
+    """codes = round_half_away(x / scale_row), scale_row = max|x_row| / 127 (quant.cpp:44-57).
+
+    ``check_finite`` mirrors quant.cpp:14-22 (reads one int64 back).
+    """
+    _require_cuda(x, torch.float32, "quantize_per_row")
+    if x.dim() < 2:
+        raise ValueError("quantize_per_row: expected a matrix [..., rows, cols]")
+    x = x.contiguous()
+    cols = x.shape[-1]
+    rows = x.numel() // cols if cols else 0
+    codes = torch.empty(x.shape, dtype=torch.int8, device=x.device)
+    scales = torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device)
+    bad = torch.full((1,), _INT64_MAX, dtype=torch.int64, device=x.device) if check_finite \
+        else None
+    lib = _lib.load()
+    _lib.check(lib.ifa_quantize_per_row(x.data_ptr(), rows, cols, codes.data_ptr(),
+                                        scales.data_ptr(),
+                                        bad.data_ptr() if bad is not None else None,
+                                        _stream_ptr(stream)))
+    if bad is not None:
+        idx = int(bad.item())
+        if idx != _INT64_MAX:
+            raise ValueError(f"quantize_per_row: non-finite input at index {idx}")
+    return QuantizedRows(codes, scales)
+
+
+def quantize_per_tensor(x: torch.Tensor, *, check_finite: bool = True,
+                        stream: Optional[torch.cuda.Stream] = None) -> QuantizedTensor:
+    """One scale max|x_slice| / 127 per trailing [rows, cols] matrix (quant.cpp:59-69)."""
+    _require_cuda(x, torch.float32, "quantize_per_tensor")
+    if x.dim() < 2:
+        raise ValueError("quantize_per_tensor: expected a matrix [..., rows, cols]")
+    x = x.contiguous()
+    rows, cols = x.shape[-2], x.shape[-1]
+    slices = x.numel() // (rows * cols) if rows * cols else math.prod(x.shape[:-2])
+    codes = torch.empty(x.shape, dtype=torch.int8, device=x.device)
+    scale = torch.empty(x.shape[:-2], dtype=torch.float32, device=x.device)
+    ws = torch.empty(max(slices, 1), dtype=torch.int32, device=x.device)
+    bad = torch.full((1,), _INT64_MAX, dtype=torch.int64, device=x.device) if check_finite \
+        else None
+    lib = _lib.load()
+    _lib.check(lib.ifa_quantize_per_tensor(x.data_ptr(), slices, rows, cols, codes.data_ptr(),
+                                           scale.data_ptr(), ws.data_ptr(),
+                                           bad.data_ptr() if bad is not None else None,
+                                           _stream_ptr(stream)))
+    if bad is not None:
+        idx = int(bad.item())
+        if idx != _INT64_MAX:
+            raise ValueError(f"quantize_per_tensor: non-finite input at index {idx}")
+    return QuantizedTensor(codes, scale)
+
+
+def int_flash_attention(inputs: QuantizedAttentionInputs,
+                        cfg: Optional[AttentionConfig] = None,
+                        audit: Optional[PCodeAudit] = None, *,
+                        out: Optional[torch.Tensor] = None,
+                        validate: bool = True,
+                        stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """Full-INT8 tiled attention (attention.hpp:82-87) on the GPU.
+
+    Returns f32 O with the shape of ``inputs.q.values``.  ``audit`` (if given)
+    is filled like the reference's PCodeAudit (one host readback).
+    ``validate=False`` skips the host-side sV check (no device sync).
+    """
+    cfg = cfg or AttentionConfig()
+    qv, kv, vv = inputs.q.values, inputs.k.values, inputs.v.values
+    for name, t in (("q", qv), ("k", kv), ("v", vv)):
+        _require_cuda(t, torch.int8, f"int_flash_attention: {name}")
+    if validate:
+        inputs.validate()
+    else:
+        if qv.dim() < 2 or qv.shape[-2] < 1 or qv.shape[-1] < 1:
+            raise ValueError("quantized attention inputs: empty q")
+    cfg.validate()
+    n, d = qv.shape[-2], qv.shape[-1]
+    slices = qv.numel() // (n * d)
+    q, k, v = qv.contiguous(), kv.contiguous(), vv.contiguous()
+    sq = inputs.q.scales.contiguous()
+    sk = inputs.k.scales.contiguous()
+    sv = inputs.v.scale.contiguous().reshape(-1)
+    if out is None:
+        out = torch.empty(qv.shape, dtype=torch.float32, device=qv.device)
+    flags = (_lib.FLAG_SQRT_D if cfg.apply_sqrt_d_scaling else 0) | \
+        (_lib.FLAG_CAUSAL if cfg.causal else 0)
+    lib = _lib.load()
+    au = None
+    sp = _stream_ptr(stream)
+    if audit is not None:
+        au = torch.empty(3, dtype=torch.int64, device=qv.device)  # 24 bytes
+        _lib.check(lib.ifa_audit_init(au.data_ptr(), sp))
+    _lib.check(lib.ifa_int_flash_fwd(q.data_ptr(), sq.data_ptr(), k.data_ptr(), sk.data_ptr(),
+                                     v.data_ptr(), sv.data_ptr(), out.data_ptr(), slices, n, d,
+                                     cfg.blocks.Br, cfg.blocks.Bc, flags,
+                                     au.data_ptr() if au is not None else None, sp))
+    if au is not None:
+        raw = au.cpu().numpy()
+        w = raw[:2].view("int32")
+        audit.min_code = int(w[0])
+        audit.max_code = int(w[1])
+        audit.row_max_block_hits_127 = bool(w[2])
+        audit.rows_audited = int(raw[2])
+    return out
+
+
+def version() -> str:
+    return _lib.load().ifa_version().decode()

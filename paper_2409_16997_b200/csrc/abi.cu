@@ -1,0 +1,156 @@
+// abi.cu -- the extern "C" boundary (include/ifa_b200.h).
+//
+// Argument validation mirrors the reference's exception behaviour
+// (attention.cpp:213-233 QuantizedAttentionInputs::validate, gemm.cpp:16-20
+// BlockSpec::validate, gemm.cpp:22-28 check_int_gemm_depth) as status codes
+// plus a thread-local message; the C++ shim (include/ifa_b200.hpp) turns
+// them back into the same exception types.  There is no CPU fallback: a
+// missing device / CUDA failure is reported as IFA_ECUDA.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "ifa_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(IFA_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// Copies [rows][d] int8 codes into [rows][pitch] with zero columns [d, pitch).
+__global__ void pad_codes_kernel(const int8_t* __restrict__ src, int8_t* __restrict__ dst,
+                                 int64_t rows, int64_t d, int64_t pitch) {
+    const int64_t total = rows * pitch;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i / pitch, c = i - r * pitch;
+        dst[i] = c < d ? src[r * d + c] : static_cast<int8_t>(0);
+    }
+}
+
+__global__ void audit_init_kernel(ifa_pcode_audit* a) {
+    a->min_code = 127;
+    a->max_code = 0;
+    a->row_max_block_hits_127 = 1;
+    a->reserved = 0;
+    a->rows_audited = 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ifa_last_error(void) { return g_err.c_str(); }
+
+const char* ifa_version(void) { return "ifa_b200 0.1 sm_100a (tcgen05 kind::i8)"; }
+
+int ifa_audit_init(ifa_pcode_audit* audit, void* stream) {
+    g_err.clear();
+    if (!audit) return fail(IFA_EINVAL, "ifa_audit_init: null audit");
+    audit_init_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(audit);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? IFA_OK : cuda_fail(e, "ifa_audit_init");
+}
+
+int ifa_quantize_per_row(const float* x, int64_t rows, int64_t cols, int8_t* codes,
+                         float* scales, int64_t* nonfinite_index, void* stream) {
+    g_err.clear();
+    if (rows < 0 || cols < 0) return fail(IFA_EINVAL, "quantize_per_row: negative matrix extent");
+    if (rows == 0 || cols == 0) return IFA_OK;
+    if (!x || !codes || !scales) return fail(IFA_EINVAL, "quantize_per_row: null pointer");
+    const cudaError_t e = ifa_b200::launch_quantize_per_row(
+        x, rows, cols, codes, scales, nonfinite_index, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? IFA_OK : cuda_fail(e, "quantize_per_row");
+}
+
+int ifa_quantize_per_tensor(const float* x, int64_t slices, int64_t rows, int64_t cols,
+                            int8_t* codes, float* slice_scales, void* workspace,
+                            int64_t* nonfinite_index, void* stream) {
+    g_err.clear();
+    if (slices < 0 || rows < 0 || cols < 0)
+        return fail(IFA_EINVAL, "quantize_per_tensor: negative matrix extent");
+    if (slices == 0) return IFA_OK;
+    if (!slice_scales || !workspace) return fail(IFA_EINVAL, "quantize_per_tensor: null pointer");
+    if (rows == 0 || cols == 0) {
+        // max_abs over an empty matrix is 0 -> scale 0 (quant.cpp:34-40, :59-69)
+        const cudaError_t e = cudaMemsetAsync(slice_scales, 0, sizeof(float) * slices,
+                                              static_cast<cudaStream_t>(stream));
+        return e == cudaSuccess ? IFA_OK : cuda_fail(e, "quantize_per_tensor");
+    }
+    if (!x || !codes) return fail(IFA_EINVAL, "quantize_per_tensor: null pointer");
+    const cudaError_t e = ifa_b200::launch_quantize_per_tensor(
+        x, slices, rows, cols, codes, slice_scales, static_cast<uint32_t*>(workspace),
+        nonfinite_index, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? IFA_OK : cuda_fail(e, "quantize_per_tensor");
+}
+
+int ifa_int_flash_fwd(const int8_t* q, const float* sq, const int8_t* k, const float* sk,
+                      const int8_t* v, const float* sv, float* o, int64_t slices, int64_t n,
+                      int64_t d, int64_t br, int64_t bc, uint32_t flags,
+                      ifa_pcode_audit* audit, void* stream) {
+    g_err.clear();
+    if (slices < 0) return fail(IFA_EINVAL, "int_flash_attention: negative slice count");
+    // attention.cpp:215-218
+    if (n < 1 || d < 1) return fail(IFA_EINVAL, "quantized attention inputs: empty q");
+    // gemm.cpp:16-20 (AttentionConfig::validate)
+    if (br < 1 || bc < 1) return fail(IFA_EINVAL, "BlockSpec: Br and Bc must be >= 1");
+    // attention.cpp:241-242 / gemm.cpp:22-28
+    if (d > IFA_MAX_INT_GEMM_DEPTH)
+        return fail(IFA_EOVERFLOW, "int gemm depth " + std::to_string(d) +
+                                       " exceeds 133144; int32 accumulation could overflow");
+    const int64_t kv_depth = bc < n ? bc : n;
+    if (kv_depth > IFA_MAX_INT_GEMM_DEPTH)
+        return fail(IFA_EOVERFLOW, "int gemm depth " + std::to_string(kv_depth) +
+                                       " exceeds 133144; int32 accumulation could overflow");
+    if (flags & ~(IFA_FLAG_SQRT_D | IFA_FLAG_CAUSAL))
+        return fail(IFA_EINVAL, "int_flash_attention: unknown flag bits");
+    if (d > 128)
+        return fail(IFA_ENOTSUP, "int_flash_attention: head dim " + std::to_string(d) +
+                                     " > 128 is not supported by the sm_100a kernel");
+    if (slices == 0) return IFA_OK;
+    if (slices > 65535)
+        return fail(IFA_ENOTSUP, "int_flash_attention: more than 65535 slices per call");
+    if (!q || !sq || !k || !sk || !v || !sv || !o)
+        return fail(IFA_EINVAL, "int_flash_attention: null pointer");
+
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ifa_b200::AttnArgs a{q, sq, k, sk, v, sv, o, audit, slices, n, d, d, bc, flags};
+    const bool aligned = (reinterpret_cast<uintptr_t>(q) % 16 == 0) &&
+                         (reinterpret_cast<uintptr_t>(k) % 16 == 0) &&
+                         (reinterpret_cast<uintptr_t>(v) % 16 == 0);
+    int8_t* padded = nullptr;
+    if (d % 16 != 0 || !aligned) {
+        // TMA needs 16-byte row pitches: stage zero-padded copies (exact for
+        // the integer dot products, gemm.hpp:12-13).
+        const int64_t pitch = (d + 15) / 16 * 16;
+        const int64_t per = slices * n * pitch;
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&padded), 3 * per, st);
+        if (e != cudaSuccess) return cuda_fail(e, "int_flash_attention: workspace");
+        const int64_t rows = slices * n;
+        const int blocks = static_cast<int>((per + 255) / 256 < 4096 ? (per + 255) / 256 : 4096);
+        pad_codes_kernel<<<blocks, 256, 0, st>>>(q, padded, rows, d, pitch);
+        pad_codes_kernel<<<blocks, 256, 0, st>>>(k, padded + per, rows, d, pitch);
+        pad_codes_kernel<<<blocks, 256, 0, st>>>(v, padded + 2 * per, rows, d, pitch);
+        a.q = padded;
+        a.k = padded + per;
+        a.v = padded + 2 * per;
+        a.pitch = pitch;
+    }
+    cudaError_t e = ifa_b200::launch_int_flash_fwd(a, st);
+    if (padded) {
+        const cudaError_t e2 = cudaFreeAsync(padded, st);
+        if (e == cudaSuccess) e = e2;
+    }
+    return e == cudaSuccess ? IFA_OK : cuda_fail(e, "int_flash_attention");
+}
+
+}  // extern "C"

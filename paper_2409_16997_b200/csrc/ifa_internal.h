@@ -1,0 +1,40 @@
+// ifa_internal.h -- launcher declarations shared by the CUDA translation
+// units of libifa_b200.so (not part of the public C-ABI, see
+// include/ifa_b200.h for that).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "../../include/ifa_b200.h"
+
+namespace ifa_b200 {
+
+cudaError_t launch_quantize_per_row(const float* x, int64_t rows, int64_t cols, int8_t* codes,
+                                    float* scales, int64_t* bad, cudaStream_t stream);
+cudaError_t launch_quantize_per_tensor(const float* x, int64_t slices, int64_t rows,
+                                       int64_t cols, int8_t* codes, float* slice_scales,
+                                       uint32_t* amax_ws, int64_t* bad, cudaStream_t stream);
+
+struct AttnArgs {
+    const int8_t* q;
+    const float* sq;
+    const int8_t* k;
+    const float* sk;
+    const int8_t* v;
+    const float* sv;
+    float* o;
+    ifa_pcode_audit* audit;  // device pointer or null
+    int64_t slices;
+    int64_t n;
+    int64_t d;       // true head dim (columns of O)
+    int64_t pitch;   // row pitch (elements) of the q/k/v code buffers, % 16 == 0
+    int64_t bc;
+    uint32_t flags;
+};
+
+// q/k/v rows have pitch `pitch` >= d with pitch % 16 == 0 (the C-ABI layer
+// makes zero-padded copies when d % 16 != 0); columns >= d must be zero.
+cudaError_t launch_int_flash_fwd(const AttnArgs& a, cudaStream_t stream);
+
+}  // namespace ifa_b200

@@ -1,0 +1,180 @@
+"""GPU parity: the sm_100a path (through the C-ABI) vs the CPU oracle.
+
+Bar: int8 codes, scales and the attention output of
+the exact kernel are compared BITWISE with the oracle restatement (which is
+itself pinned bitwise to the unmodified reference in test_oracle.py); the
+audit must match field by field.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(a):
+    a = np.asarray(a)
+    if a.ndim == 0:
+        return torch.tensor(a.item(), dtype=torch.float32, device="cuda")
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _gpu_attention(ifa, qc, qs, kc, ks, vc, vs, br, bc, causal=False, sqrt_d=False,
+                   audit=False):
+    inputs = ifa.QuantizedAttentionInputs(
+        ifa.QuantizedRows(_dev(qc), _dev(qs)), ifa.QuantizedRows(_dev(kc), _dev(ks)),
+        ifa.QuantizedTensor(_dev(vc), _dev(np.asarray(vs, np.float32))))
+    cfg = ifa.AttentionConfig(ifa.BlockSpec(br, bc), apply_sqrt_d_scaling=sqrt_d,
+                              causal=causal)
+    au = ifa.PCodeAudit() if audit else None
+    out = ifa.int_flash_attention(inputs, cfg, au).cpu().numpy()
+    if audit:
+        return out, (au.min_code, au.max_code, au.row_max_block_hits_127, au.rows_audited)
+    return out
+
+
+def _quantized_case(oracle, dist, n, d, seed):
+    q, k, v = oracle.slice_inputs(dist, n, d, seed=seed)
+    qc, qs = oracle.quantize_per_row(q)
+    kc, ks = oracle.quantize_per_row(k)
+    vc, vs = oracle.quantize_per_tensor(v)
+    return (q, k, v), (qc, qs, kc, ks, vc, vs)
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+# ---------------------------------------------------------------- quantize
+@pytest.mark.parametrize("rows,cols", [(1, 1), (3, 7), (64, 64), (257, 128), (100, 100),
+                                       (33, 256), (5, 513), (4096, 128)])
+@pytest.mark.parametrize("dist", ["normal", "uniform"])
+def test_quantize_per_row_bitwise(ifa, oracle, rows, cols, dist):
+    x = oracle.generate(dist, rows, cols, seed=rows * 1000 + cols)
+    x[0, :] = 0.0                       # all-zero row -> scale 0, codes 0
+    if rows > 2:
+        x[2, :] *= 1e-30                # tiny magnitudes
+    want_c, want_s = oracle.quantize_per_row(x)
+    got = ifa.quantize_per_row(_dev(x))
+    assert np.array_equal(got.values.cpu().numpy(), want_c)
+    assert np.array_equal(_bits(got.scales.cpu().numpy()), _bits(want_s))
+
+
+@pytest.mark.parametrize("slices,rows,cols", [(1, 1, 1), (3, 17, 5), (4, 128, 64),
+                                              (8, 1024, 128)])
+def test_quantize_per_tensor_bitwise(ifa, oracle, slices, rows, cols):
+    x = np.stack([oracle.generate("normal", rows, cols, seed=s + 7) * (10.0 ** (s % 3))
+                  for s in range(slices)])
+    got = ifa.quantize_per_tensor(_dev(x))
+    for s in range(slices):
+        wc, ws = oracle.quantize_per_tensor(x[s])
+        assert np.array_equal(got.values[s].cpu().numpy(), wc)
+        assert _bits(got.scale[s].cpu().numpy()) == _bits(ws)
+
+
+def test_quantize_rejects_nonfinite_with_index(ifa):
+    x = torch.tensor([[1.0, 2.0], [float("inf"), 4.0]], device="cuda")
+    with pytest.raises(ValueError, match="index 2"):
+        ifa.quantize_per_row(x)
+    x[1, 0] = float("nan")
+    with pytest.raises(ValueError, match="index 2"):
+        ifa.quantize_per_tensor(x)
+
+
+def test_quantize_worked_examples(ifa):
+    q = ifa.quantize_per_row(torch.tensor([[2.0, -1.0, 0.5]], device="cuda"))
+    assert q.values.cpu().tolist() == [[127, -64, 32]]          # test_quant.cpp:16-23
+    assert q.scales.item() == np.float32(2.0) / np.float32(127.0)
+    t = ifa.quantize_per_tensor(torch.tensor([[1.0, -2.0], [4.0, 0.5]], device="cuda"))
+    assert t.values.cpu().tolist() == [[32, -64], [127, 16]]    # test_quant.cpp:25-33
+
+
+# ---------------------------------------------------------------- attention
+SHAPES = [(1, 1), (5, 8), (24, 16), (33, 8), (40, 16), (128, 128), (200, 64), (300, 100),
+          (1024, 64), (1000, 128)]
+
+
+@pytest.mark.parametrize("n,d", SHAPES)
+@pytest.mark.parametrize("dist", ["normal", "uniform"])
+def test_attention_bitwise_vs_oracle(ifa, oracle, n, d, dist):
+    _, (qc, qs, kc, ks, vc, vs) = _quantized_case(oracle, dist, n, d, seed=n * 31 + d)
+    for bc in sorted({64, 128, n, max(1, n // 3)}):
+        want, want_audit = oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, bc,
+                                                      audit=True)
+        got, got_audit = _gpu_attention(ifa, qc, qs, kc, ks, vc, vs, 64, bc, audit=True)
+        assert np.array_equal(_bits(got), _bits(want)), (n, d, bc,
+                                                          float(np.abs(got - want).max()))
+        assert got_audit == want_audit, (n, d, bc)
+
+
+@pytest.mark.parametrize("n,d,bc", [(40, 8, 3), (33, 16, 5), (130, 32, 7), (257, 64, 200),
+                                    (600, 128, 300), (300, 128, 1)])
+def test_attention_odd_blocks_bitwise(ifa, oracle, n, d, bc):
+    _, (qc, qs, kc, ks, vc, vs) = _quantized_case(oracle, "uniform", n, d, seed=bc)
+    want = oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, bc)
+    got = _gpu_attention(ifa, qc, qs, kc, ks, vc, vs, 64, bc)
+    assert np.array_equal(_bits(got), _bits(want))
+
+
+@pytest.mark.parametrize("n,d,bc", [(1, 8, 64), (37, 16, 8), (300, 64, 128), (700, 128, 128),
+                                    (513, 128, 1000), (256, 64, 64)])
+@pytest.mark.parametrize("dist", ["normal", "uniform"])
+def test_attention_causal_bitwise(ifa, oracle, n, d, bc, dist):
+    _, (qc, qs, kc, ks, vc, vs) = _quantized_case(oracle, dist, n, d, seed=n + d)
+    want, wa = oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, bc, flags=2, audit=True)
+    got, ga = _gpu_attention(ifa, qc, qs, kc, ks, vc, vs, 64, bc, causal=True, audit=True)
+    assert np.array_equal(_bits(got), _bits(want))
+    assert ga == wa
+
+
+def test_attention_sqrt_d_bitwise(ifa, oracle):
+    _, (qc, qs, kc, ks, vc, vs) = _quantized_case(oracle, "normal", 333, 128, seed=5)
+    want = oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, 128, flags=1)
+    got = _gpu_attention(ifa, qc, qs, kc, ks, vc, vs, 64, 128, sqrt_d=True)
+    assert np.array_equal(_bits(got), _bits(want))
+
+
+def test_one_by_one_case_is_exact(ifa):
+    # test_attention.cpp:219-235
+    out, audit = _gpu_attention(ifa, np.array([[5]], np.int8), np.array([0.3], np.float32),
+                                np.array([[-7]], np.int8), np.array([0.1], np.float32),
+                                np.array([[23]], np.int8), np.float32(0.25), 64, 64,
+                                audit=True)
+    assert out[0, 0] == np.float32(5.75)
+    assert audit == (127, 127, True, 1)
+
+
+def test_batched_slices_bitwise(ifa, oracle):
+    n, d, slices = 512, 128, 6
+    qs_, ks_, vs_, qc_, kc_, vc_, sv_ = [], [], [], [], [], [], []
+    for s in range(slices):
+        q, k, v = oracle.slice_inputs("uniform" if s % 2 else "normal", n, d, b=s // 2, h=s % 2)
+        a, b = oracle.quantize_per_row(q)
+        c, e = oracle.quantize_per_row(k)
+        f, g = oracle.quantize_per_tensor(v)
+        qc_.append(a), qs_.append(b), kc_.append(c), ks_.append(e), vc_.append(f), sv_.append(g)
+    qc, qs, kc, ks, vc = map(np.stack, (qc_, qs_, kc_, ks_, vc_))
+    sv = np.array(sv_, np.float32)
+    want = oracle.int_flash_attention_batched(qc, qs, kc, ks, vc, sv, 64, 128)
+    got = _gpu_attention(ifa, qc, qs, kc, ks, vc, sv, 64, 128)
+    assert np.array_equal(_bits(got), _bits(want))
+
+
+def test_validation_errors(ifa):
+    i8 = lambda *s: torch.zeros(*s, dtype=torch.int8, device="cuda")
+    f32 = lambda *s: torch.ones(*s, dtype=torch.float32, device="cuda")
+    good = ifa.QuantizedAttentionInputs(ifa.QuantizedRows(i8(4, 4), f32(4)),
+                                        ifa.QuantizedRows(i8(4, 4), f32(4)),
+                                        ifa.QuantizedTensor(i8(4, 4), f32(())))
+    bad_k = ifa.QuantizedAttentionInputs(good.q, ifa.QuantizedRows(i8(4, 3), f32(4)), good.v)
+    with pytest.raises(ValueError):
+        ifa.int_flash_attention(bad_k)
+    bad_s = ifa.QuantizedAttentionInputs(ifa.QuantizedRows(i8(4, 4), f32(3)), good.k, good.v)
+    with pytest.raises(ValueError):
+        ifa.int_flash_attention(bad_s)
+    bad_v = ifa.QuantizedAttentionInputs(good.q, good.k,
+                                         ifa.QuantizedTensor(i8(4, 4), -f32(())))
+    with pytest.raises(ValueError):
+        ifa.int_flash_attention(bad_v)
+    with pytest.raises(ValueError):
+        ifa.int_flash_attention(good, ifa.AttentionConfig(ifa.BlockSpec(0, 4)))
