@@ -1,0 +1,108 @@
+"""Pre-planned execution of the whole hot path (quantize Q, K, V + INT8
+flash attention) for a fixed [slices, n, d] shape.
+
+``AttentionPlan`` owns every device buffer the path needs (codes, scales,
+V-absmax workspace, non-finite detector, output) so a step is four C-ABI
+calls on one stream with no allocation and no host synchronisation; the
+reference's non-finite rejection (quant.cpp:14-22) is folded into a device
+word that ``check()`` reads once.  ``capture()`` records a step into a CUDA
+graph for launch-bound (small) shapes.  This is the executor ``bench.py``
+and multi-GPU runs use; the per-call API in ``api.py`` is the drop-in
+mirror of the reference functions.
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+
+from . import _lib
+
+_INT64_MAX = (1 << 63) - 1
+
+
+class AttentionPlan:
+    def __init__(self, slices: int, n: int, d: int, *, bc: int = 128, br: int = 128,
+                 causal: bool = False, sqrt_d: bool = False,
+                 device: Optional[torch.device] = None):
+        if slices < 1 or n < 1 or d < 1:
+            raise ValueError("AttentionPlan: slices, n and d must be >= 1")
+        if bc < 1 or br < 1:
+            raise ValueError("BlockSpec: Br and Bc must be >= 1")
+        self.lib = _lib.load()
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.device = dev
+        self.slices, self.n, self.d, self.bc, self.br = slices, n, d, bc, br
+        self.flags = (_lib.FLAG_CAUSAL if causal else 0) | (_lib.FLAG_SQRT_D if sqrt_d else 0)
+        shape = (slices, n, d)
+        self.qc = torch.empty(shape, dtype=torch.int8, device=dev)
+        self.kc = torch.empty(shape, dtype=torch.int8, device=dev)
+        self.vc = torch.empty(shape, dtype=torch.int8, device=dev)
+        self.sq = torch.empty((slices, n), dtype=torch.float32, device=dev)
+        self.sk = torch.empty((slices, n), dtype=torch.float32, device=dev)
+        self.sv = torch.empty((slices,), dtype=torch.float32, device=dev)
+        self.out = torch.empty(shape, dtype=torch.float32, device=dev)
+        self.ws = torch.empty((slices,), dtype=torch.int32, device=dev)
+        self.bad = torch.full((1,), _INT64_MAX, dtype=torch.int64, device=dev)
+        self.graph: Optional[torch.cuda.CUDAGraph] = None
+        self._graph_io = None
+
+    # ------------------------------------------------------------------
+    def quantize(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                 stream: Optional[torch.cuda.Stream] = None) -> None:
+        s = int((stream or torch.cuda.current_stream(self.device)).cuda_stream)
+        L, rows, d = self.lib, self.slices * self.n, self.d
+        bad = self.bad.data_ptr()
+        _lib.check(L.ifa_quantize_per_row(q.data_ptr(), rows, d, self.qc.data_ptr(),
+                                          self.sq.data_ptr(), bad, s))
+        _lib.check(L.ifa_quantize_per_row(k.data_ptr(), rows, d, self.kc.data_ptr(),
+                                          self.sk.data_ptr(), bad, s))
+        _lib.check(L.ifa_quantize_per_tensor(v.data_ptr(), self.slices, self.n, d,
+                                             self.vc.data_ptr(), self.sv.data_ptr(),
+                                             self.ws.data_ptr(), bad, s))
+
+    def attention(self, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        s = int((stream or torch.cuda.current_stream(self.device)).cuda_stream)
+        _lib.check(self.lib.ifa_int_flash_fwd(
+            self.qc.data_ptr(), self.sq.data_ptr(), self.kc.data_ptr(), self.sk.data_ptr(),
+            self.vc.data_ptr(), self.sv.data_ptr(), self.out.data_ptr(), self.slices, self.n,
+            self.d, self.br, self.bc, self.flags, None, s))
+        return self.out
+
+    def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """quantize_per_row(Q), quantize_per_row(K), quantize_per_tensor(V) per
+        slice, then int_flash_attention; inputs f32 [slices, n, d] on device."""
+        for t in (q, k, v):
+            if t.dtype != torch.float32 or not t.is_contiguous() or \
+                    tuple(t.shape) != (self.slices, self.n, self.d) or t.device != self.device:
+                raise ValueError("AttentionPlan.forward: expected contiguous f32 "
+                                 f"{(self.slices, self.n, self.d)} tensors on {self.device}")
+        self.quantize(q, k, v, stream)
+        return self.attention(stream)
+
+    def check(self) -> None:
+        """Raise like the reference if any quantized input was non-finite."""
+        idx = int(self.bad.item())
+        if idx != _INT64_MAX:
+            self.bad.fill_(_INT64_MAX)
+            raise ValueError(f"quantize: non-finite input at index {idx}")
+
+    # ------------------------------------------------------------------
+    def capture(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor) -> None:
+        """Record forward(q, k, v) into a CUDA graph (replay with ``replay()``)."""
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self.forward(q, k, v, s)  # warm-up outside the graph (lazy init)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.forward(q, k, v)
+        self.graph = g
+        self._graph_io = (q, k, v)
+
+    def replay(self) -> torch.Tensor:
+        assert self.graph is not None, "capture() first"
+        self.graph.replay()
+        return self.out
