@@ -12,7 +12,7 @@ CSRC := $(PKG)/csrc
 LIB := $(PKG)/lib/libifa_b200.so
 SRCS := $(CSRC)/abi.cu $(CSRC)/attn.cu $(CSRC)/quant.cu
 HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/ifa_internal.h include/ifa_b200.h
-NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
+NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=false \
            -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 
 all: $(LIB) oracle

@@ -13,18 +13,24 @@
 // plus the PCodeAudit bookkeeping (:309-311, :319-326, :343-355) and the
 // causal extension (keys j <= row i only).
 //
-// One CTA owns a 128-row Q tile of one (b,h) slice.  Warp roles:
-//   warp 0      TMA producer: Q once, then a STAGES-deep ring of K / V tiles
-//               (128 keys x D int8, 128B or 64B swizzle) + the K scales.
-//   warp 1      MMA issuer (one thread): S = Q.K^T  (tcgen05.mma kind::i8,
-//               A and B from SMEM) into TMEM; PV = P.V (A = P from TMEM,
-//               B = V from SMEM, MN-major) into TMEM.
-//   warp 2      TMEM allocator.
-//   warps 4-7   softmax: thread r owns Q row r (= TMEM lane r); reads the
-//               int32 S row with tcgen05.ld, dequantizes, row max, exact
-//               expf-based requantization of P to int8, writes P to TMEM.
-//   warps 8-11  correction: acc = acc*alpha + float(PV) on the f32
-//               accumulator kept in TMEM; final O = (acc/l)*sV epilogue.
+// One CTA owns a 128-row Q tile of one (b,h) slice.  Warp roles (16 warps):
+//   warp 0       TMA producer: Q once, then a STAGES-deep ring of K / V tiles
+//                (128 keys x D int8, 128B/64B swizzle) + the K scales.
+//   warp 1       MMA issuer (one thread): S = Q.K^T (tcgen05.mma kind::i8,
+//                A and B from SMEM) into TMEM; PV = P.V (A = P from TMEM,
+//                B = V from SMEM, MN-major) into TMEM.
+//   warp 2       TMEM allocator.
+//   warps 4-11   softmax: two threads per Q row (TMEM lane), each owning 64
+//                of the 128 key columns; tcgen05.ld the int32 S half-row,
+//                dequantize, exchange the half-row max through SMEM, exact
+//                requantization of P (MUFU estimate + rounding guard, exact
+//                glibc-expf fallback), tcgen05.st the packed int8 codes.
+//   warps 12-15  correction: acc = acc*alpha + float(PV) on the f32
+//                accumulator kept in TMEM, l = l*alpha + sum(P); final
+//                O = (acc/l)*sV epilogue.
+// Elementwise math uses sm_100 packed FADD2/FMUL2/FFMA2 (IEEE RN per lane,
+// bit-identical to the scalar ops) and magic-number int<->float conversion
+// so the XU (conversion/MUFU) pipe only carries the EX2.
 // TMEM columns: S [0,128) | PV [128,256) | ACC [256,384) | P0 [384,416) |
 // P1 [416,448).
 //
@@ -51,9 +57,18 @@ namespace attn {
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int STAGES = 3;
-constexpr int NUM_THREADS = 384;
+constexpr int NUM_THREADS = 512;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t T_S = 0, T_PV = 128, T_ACC = 256, T_P0 = 384;
+constexpr float kMagic = 12582912.0f;       // 1.5 * 2^23: float(i) = bits(i + M) - M
+constexpr int32_t kMagicBits = 0x4B400000;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLog2_127 = 6.9886846867721655f;
+// MUFU estimate of y = 127*e^x is within 1.6e-4 of fl(127*fl(expf(x)))
+// (|t| <= 7 rounding 2^-22 + log2e/log2(127) constants 2^-22 + ex2.approx
+// 2^-21 relative); codes whose estimate lies within kGuard of a rounding
+// boundary are recomputed exactly.
+constexpr float kGuardThresh = 0.5f - 2.5e-4f;
 
 enum ItemKind : uint32_t {
     K_MAXONLY = 1u,   // pass-1 sub-tile of a multi-tile block: contributes to the row max
@@ -111,21 +126,25 @@ struct ItemGen {
     }
 };
 
+struct RingEntry {
+    float alpha[BM];
+    int32_t psum[2][BM];
+};
+
 template <int D>
 struct alignas(1024) Smem {
     uint8_t q[BM * D];
     uint8_t k[STAGES][BN * D];
     uint8_t v[STAGES][BN * D];
     float sk[STAGES][BN];
-    float alpha[4][BM];
-    float lfin[BM];
+    float xmax[2][2][BM];  // [item parity][half][row]: half-row max exchange
+    RingEntry ring[4];     // per-block alpha and code sums for the correction warps
     uint64_t q_full;
     uint64_t k_full[STAGES], v_full[STAGES], kv_empty[STAGES];
     uint64_t s_full, s_empty;
     uint64_t p_full[2], p_empty[2];
     uint64_t pv_full, pv_empty;
-    uint64_t alpha_full[4];
-    uint64_t l_full;
+    uint64_t ring_full[4];
     uint32_t tmem_base;
 };
 
@@ -143,9 +162,48 @@ struct Params {
     int32_t q_tiles;
 };
 
-__device__ __forceinline__ float warp_min_i(float v) { return v; }
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
-template <int D>
+// Requantize 8 consecutive scores: packed codes (2 words) for
+// round(127*expf(s - m_new)); returns the code sum via dp4a into psum.
+__device__ __forceinline__ void codes8(const float* s, float m_new, uint32_t* w,
+                                       int32_t& psum) {
+    float x[8], r[8], df[8];
+    const float2 negm = f2(-m_new);
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+        const float2 xx = fadd2(make_float2(s[e], s[e + 1]), negm);
+        const float2 t = ffma2(xx, f2(kLog2e), f2(kLog2_127));
+        const float2 y = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+        const float2 rr = fadd2(y, f2(kMagic));
+        const float2 rf = fsub2(rr, f2(kMagic));
+        const float2 d2 = fsub2(y, rf);
+        x[e] = xx.x;
+        x[e + 1] = xx.y;
+        r[e] = rr.x;
+        r[e + 1] = rr.y;
+        df[e] = d2.x;
+        df[e + 1] = d2.y;
+    }
+    const float g = fmaxf(fmax3(fmax3(fabsf(df[0]), fabsf(df[1]), fabsf(df[2])),
+                                fmax3(fabsf(df[3]), fabsf(df[4]), fabsf(df[5])), fabsf(df[6])),
+                          fabsf(df[7]));
+    if (g > kGuardThresh) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            r[e] = __int_as_float(kMagicBits + exact_code(x[e]));
+    }
+    w[0] = __byte_perm(__byte_perm(__float_as_uint(r[0]), __float_as_uint(r[1]), 0x0040),
+                       __byte_perm(__float_as_uint(r[2]), __float_as_uint(r[3]), 0x0040),
+                       0x5410);
+    w[1] = __byte_perm(__byte_perm(__float_as_uint(r[4]), __float_as_uint(r[5]), 0x0040),
+                       __byte_perm(__float_as_uint(r[6]), __float_as_uint(r[7]), 0x0040),
+                       0x5410);
+    psum = static_cast<int32_t>(__dp4a(w[0], 0x01010101u, static_cast<uint32_t>(psum)));
+    psum = static_cast<int32_t>(__dp4a(w[1], 0x01010101u, static_cast<uint32_t>(psum)));
+}
+
+template <int D, bool AUDIT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     int_flash_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_k,
@@ -155,6 +213,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     constexpr uint32_t kTileBytes = BN * D;
     constexpr uint32_t kIdescS = idesc_i8(BM, BN, false, false);
     constexpr uint32_t kIdescPV = idesc_i8(BM, D, false, true);
+    const float kNegInf = -__int_as_float(0x7f800000);
 
     extern __shared__ uint8_t smem_raw[];
     Smem<D>& sm = *reinterpret_cast<Smem<D>*>(
@@ -177,18 +236,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int i = 0; i < STAGES; ++i) {
             mbar_init(&sm.k_full[i], 32);
             mbar_init(&sm.v_full[i], 1);
-            mbar_init(&sm.kv_empty[i], 1 + 4);
+            mbar_init(&sm.kv_empty[i], 1 + 8);
         }
         mbar_init(&sm.s_full, 1);
-        mbar_init(&sm.s_empty, 4);
+        mbar_init(&sm.s_empty, 8);
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&sm.p_full[i], 4);
+            mbar_init(&sm.p_full[i], 8);
             mbar_init(&sm.p_empty[i], 1);
         }
         mbar_init(&sm.pv_full, 1);
         mbar_init(&sm.pv_empty, 4);
-        for (int i = 0; i < 4; ++i) mbar_init(&sm.alpha_full[i], 4);
-        mbar_init(&sm.l_full, 4);
+        for (int i = 0; i < 4; ++i) mbar_init(&sm.ring_full[i], 8);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<TMEM_COLS>(&sm.tmem_base);
@@ -216,11 +274,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         while (gen.next(it)) {
             const uint32_t st = i % STAGES;
             if (i >= STAGES) mbar_wait(&sm.kv_empty[st], ((i / STAGES) - 1) & 1);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int64_t key = it.key0 + lane * 4 + e;
-                sm.sk[st][lane * 4 + e] = key < n ? sk_slice[key] : 0.0f;
+            float4 kv4;
+            const int64_t key = it.key0 + lane * 4;
+            if (key + 3 < n && (reinterpret_cast<uintptr_t>(sk_slice + key) & 15) == 0) {
+                kv4 = __ldg(reinterpret_cast<const float4*>(sk_slice + key));
+            } else {
+                kv4.x = key + 0 < n ? sk_slice[key + 0] : 0.0f;
+                kv4.y = key + 1 < n ? sk_slice[key + 1] : 0.0f;
+                kv4.z = key + 2 < n ? sk_slice[key + 2] : 0.0f;
+                kv4.w = key + 3 < n ? sk_slice[key + 3] : 0.0f;
             }
+            reinterpret_cast<float4*>(sm.sk[st])[lane] = kv4;
             if (lane == 0) {
                 mbar_arrive_expect_tx(&sm.k_full[st], kTileBytes);
                 tma_load_3d(sm.k[st], &tm_k, &sm.k_full[st], 0, static_cast<int32_t>(it.key0),
@@ -300,21 +364,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (have_prev) issue_pv(prev_st, prev_ph, prev_kind, prev_pi);
         }
         __syncwarp();
-    } else if (warp >= 4 && warp < 8) {
+    } else if (warp >= 4 && warp < 12) {
         // ------------------------------------------------------------ softmax
-        const uint32_t quarter = warp - 4;
+        const uint32_t quarter = warp & 3;
+        const uint32_t half = (warp - 4) >> 2;
         const int32_t row = static_cast<int32_t>(quarter * 32 + lane);
         const int64_t grow = q0 + row;
         const bool row_ok = grow < n;
         const float sq_r = row_ok ? p.sq[slice * n + grow] : 0.0f;
         const uint32_t t_lane = tmem + ((quarter * 32) << 16);
+        const uint32_t c_base = 64 * half;  // first key column owned by this thread
+        const uint32_t bar_id = 1 + quarter;
         const float extra = p.extra;
-        float m = -__int_as_float(0x7f800000);
-        float l = 0.0f;
-        float blk_max = m, m_new = m, alpha = 0.0f;
+        float m = kNegInf;
+        float blk_max = kNegInf, m_new = kNegInf, alpha = 0.0f;
         int32_t p_sum = 0;
-        bool has_full = false;
-        bool row_hit = false;
+        bool has_full = false, row_hit = false;
         int32_t cmin = 127, cmax = 0;
         ItemGen gen(n, p.bc, kv_limit);
         Item it;
@@ -323,10 +388,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t st = i % STAGES;
             mbar_wait(&sm.s_full, i & 1);
             tc_fence_after();
-            uint32_t sr[BN];
-#pragma unroll
-            for (int c = 0; c < BN; c += 32)
-                tmem_ld32(t_lane + T_S + c, *reinterpret_cast<uint32_t(*)[32]>(&sr[c]));
+            uint32_t sr[64];
+            tmem_ld32(t_lane + T_S + c_base, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+            tmem_ld32(t_lane + T_S + c_base + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
@@ -338,102 +402,108 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const int64_t vis = grow - it.key0 + 1;
                 if (vis < lim) lim = vis < 0 ? 0 : static_cast<int32_t>(vis);
             }
+            lim -= static_cast<int32_t>(c_base);  // columns of this half still visible
             // dequantize: s = float(S) * (sQ * sK) [* extra], product of scales first
-            float m_loc = -__int_as_float(0x7f800000);
-            const float4* sk4 = reinterpret_cast<const float4*>(sm.sk[st]);
+            float s[64];
+            float m_loc = kNegInf, s_min = -kNegInf;
+            const float4* sk4 = reinterpret_cast<const float4*>(sm.sk[st] + c_base);
 #pragma unroll
-            for (int c4 = 0; c4 < BN / 4; ++c4) {
+            for (int c4 = 0; c4 < 16; ++c4) {
                 const float4 k4 = sk4[c4];
-                const float kv[4] = {k4.x, k4.y, k4.z, k4.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int c = c4 * 4 + e;
-                    float s = __fmul_rn(__int2float_rn(static_cast<int32_t>(sr[c])),
-                                        __fmul_rn(sq_r, kv[e]));
-                    if (extra != 1.0f) s = __fmul_rn(s, extra);
-                    s = c < lim ? s : -__int_as_float(0x7f800000);
-                    m_loc = fmaxf(m_loc, s);
-                    sr[c] = __float_as_uint(s);
+                const int c = c4 * 4;
+                const float2 sf01 = fsub2(
+                    make_float2(__int_as_float(static_cast<int32_t>(sr[c]) + kMagicBits),
+                                __int_as_float(static_cast<int32_t>(sr[c + 1]) + kMagicBits)),
+                    f2(kMagic));
+                const float2 sf23 = fsub2(
+                    make_float2(__int_as_float(static_cast<int32_t>(sr[c + 2]) + kMagicBits),
+                                __int_as_float(static_cast<int32_t>(sr[c + 3]) + kMagicBits)),
+                    f2(kMagic));
+                float2 s01 = fmul2(sf01, fmul2(f2(sq_r), make_float2(k4.x, k4.y)));
+                float2 s23 = fmul2(sf23, fmul2(f2(sq_r), make_float2(k4.z, k4.w)));
+                if (extra != 1.0f) {
+                    s01 = fmul2(s01, f2(extra));
+                    s23 = fmul2(s23, f2(extra));
                 }
+                s[c] = s01.x;
+                s[c + 1] = s01.y;
+                s[c + 2] = s23.x;
+                s[c + 3] = s23.y;
+            }
+            if (lim < 64) {
+#pragma unroll
+                for (int c = 0; c < 64; ++c) s[c] = c < lim ? s[c] : kNegInf;
+            }
+#pragma unroll
+            for (int c = 0; c < 64; c += 4) m_loc = fmax3(m_loc, fmax3(s[c], s[c + 1], s[c + 2]), s[c + 3]);
+            if (AUDIT) {
+#pragma unroll
+                for (int c = 0; c < 64; ++c)
+                    if (c < lim) s_min = fminf(s_min, s[c]);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.kv_empty[st]);
+            // half-row max exchange with the partner thread (other half, same row)
+            sm.xmax[i & 1][half][row] = m_loc;
+            named_bar_sync(bar_id, 64);
+            m_loc = fmaxf(m_loc, sm.xmax[i & 1][half ^ 1][row]);
 
-            if (it.kind & K_BEGIN) blk_max = -__int_as_float(0x7f800000);
+            if (it.kind & K_BEGIN) blk_max = kNegInf;
             if (!(it.kind & K_PV) || (it.kind & K_BEGIN)) blk_max = fmaxf(blk_max, m_loc);
             if (it.kind & K_MAXDONE) {
                 m_new = (m < blk_max) ? blk_max : m;  // std::max(m, m_loc)
                 alpha = exact_expf(__fsub_rn(m, m_new));
                 p_sum = 0;
-                has_full = false;
+                // the block's largest code comes from its largest score
+                has_full = blk_max != kNegInf && guarded_code(__fsub_rn(blk_max, m_new)) == 127;
             }
             if (it.kind & K_PV) {
-                if (it.kind & K_END) {
-                    // l / alpha for the correction warps are final only after the
-                    // codes; alpha is already known, publish it first.
-                    sm.alpha[bi & 3][row] = alpha;
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&sm.alpha_full[bi & 3]);
-                }
                 if (pi >= 2) {
                     mbar_wait(&sm.p_empty[pi & 1], ((pi - 2) >> 1) & 1);
                     tc_fence_after();
                 }
-                const uint32_t p_col = T_P0 + 32 * (pi & 1);
+                uint32_t w[16];
+                int32_t ps = 0;
 #pragma unroll
-                for (int c0 = 0; c0 < BN; c0 += 32) {
-                    uint32_t w[8];
+                for (int g = 0; g < 8; ++g) codes8(&s[8 * g], m_new, &w[2 * g], ps);
+                p_sum += ps;
+                tmem_st16(t_lane + T_P0 + 32 * (pi & 1) + 16 * half, w);
+                if (AUDIT && row_ok && lim > 0) {
+                    float my_max = kNegInf;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        uint32_t packed = 0;
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const int c = c0 + j * 4 + e;
-                            int code = 0;
-                            if (c < lim) {
-                                code = guarded_code(__fsub_rn(__uint_as_float(sr[c]), m_new));
-                                p_sum += code;
-                                has_full = has_full || code == 127;
-                                cmin = min(cmin, code);
-                                cmax = max(cmax, code);
-                            }
-                            packed |= static_cast<uint32_t>(code) << (8 * e);
-                        }
-                        w[j] = packed;
-                    }
-                    asm volatile(
-                        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
-                            t_lane + p_col + c0 / 4),
-                        "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]),
-                        "r"(w[7])
-                        : "memory");
+                    for (int c = 0; c < 64; c += 4)
+                        my_max = fmax3(my_max, fmax3(s[c], s[c + 1], s[c + 2]), s[c + 3]);
+                    cmax = max(cmax, guarded_code(__fsub_rn(my_max, m_new)));
+                    cmin = min(cmin, guarded_code(__fsub_rn(s_min, m_new)));
                 }
-                tmem_wait_st();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.p_full[pi & 1]);
                 if (it.kind & K_END) {
-                    l = __fadd_rn(__fmul_rn(l, alpha), static_cast<float>(p_sum));
+                    RingEntry& re = sm.ring[bi & 3];
+                    if (half == 0) re.alpha[row] = alpha;
+                    re.psum[half][row] = p_sum;
                     if (m_new > m)
                         row_hit = has_full;
                     else if (blk_max == m_new && has_full)
                         row_hit = true;
                     m = m_new;
-                    ++bi;
                 }
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&sm.p_full[pi & 1]);
+                    if (it.kind & K_END) mbar_arrive(&sm.ring_full[bi & 3]);
+                }
+                if (it.kind & K_END) ++bi;
                 ++pi;
             }
             ++i;
         }
-        sm.lfin[row] = l;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.l_full);
-        if (p.audit != nullptr) {
-            // rows >= n and rows with no visible key never emitted a code
+        if (AUDIT && p.audit != nullptr) {
+            // rows >= n never emitted a code; the half-1 thread reports codes only
             int32_t my_min = row_ok ? cmin : 127;
             int32_t my_max = row_ok ? cmax : 0;
-            int32_t my_hit = row_ok ? (row_hit ? 1 : 0) : 1;
-            int32_t my_rows = row_ok ? 1 : 0;
+            int32_t my_hit = (row_ok && half == 0) ? (row_hit ? 1 : 0) : 1;
+            int32_t my_rows = (row_ok && half == 0) ? 1 : 0;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 my_min = min(my_min, __shfl_xor_sync(0xffffffffu, my_min, o));
@@ -441,27 +511,57 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 my_hit = my_hit & __shfl_xor_sync(0xffffffffu, my_hit, o);
                 my_rows += __shfl_xor_sync(0xffffffffu, my_rows, o);
             }
-            if (lane == 0 && my_rows > 0) {
-                atomicMin(&p.audit->min_code, my_min);
-                atomicMax(&p.audit->max_code, my_max);
+            if (lane == 0) {
+                if (my_min < 127) atomicMin(&p.audit->min_code, my_min);
+                if (my_max > 0) atomicMax(&p.audit->max_code, my_max);
                 if (!my_hit) atomicAnd(&p.audit->row_max_block_hits_127, 0);
-                atomicAdd(reinterpret_cast<unsigned long long*>(&p.audit->rows_audited),
-                          static_cast<unsigned long long>(my_rows));
+                if (my_rows)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(&p.audit->rows_audited),
+                              static_cast<unsigned long long>(my_rows));
             }
         }
-    } else if (warp >= 8) {
+    } else if (warp >= 12) {
         // ------------------------------------------------------------ correction
-        const uint32_t quarter = warp - 8;
+        const uint32_t quarter = warp & 3;
         const int32_t row = static_cast<int32_t>(quarter * 32 + lane);
         const int64_t grow = q0 + row;
         const uint32_t t_lane = tmem + ((quarter * 32) << 16);
+        // P.V int32 of one block fits the magic conversion while |pv| < 2^22
+        const bool pv_magic = p.bc <= 256;
+        float l = 0.0f;
         ItemGen gen(n, p.bc, kv_limit);
         Item it;
         uint32_t bi = 0;
         while (gen.next(it)) {
             if (!(it.kind & K_END)) continue;
-            mbar_wait(&sm.alpha_full[bi & 3], (bi >> 2) & 1);
-            const float alpha = sm.alpha[bi & 3][row];
+            mbar_wait(&sm.ring_full[bi & 3], (bi >> 2) & 1);
+            const RingEntry& re = sm.ring[bi & 3];
+            const float alpha = re.alpha[row];
+            const int32_t psum = re.psum[0][row] + re.psum[1][row];
+            l = __fadd_rn(__fmul_rn(l, alpha), static_cast<float>(psum));
+            // acc *= alpha (attention.cpp:316-318) -- its own TMEM round trip so
+            // the product is rounded before the add (ptxas contracts adjacent
+            // mul.rn.f32x2/add.rn.f32x2 into FFMA2); skipped when alpha == 1
+            // for the whole warp, which leaves acc bit-identical.
+            if (bi > 0 && !__all_sync(0xffffffffu, alpha == 1.0f)) {
+#pragma unroll
+                for (int c0 = 0; c0 < D; c0 += 32) {
+                    uint32_t acc[32];
+                    tmem_ld32(t_lane + T_ACC + c0, acc);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 32; j += 2) {
+                        const float2 a = fmul2(make_float2(__uint_as_float(acc[j]),
+                                                           __uint_as_float(acc[j + 1])),
+                                               f2(alpha));
+                        acc[j] = __float_as_uint(a.x);
+                        acc[j + 1] = __float_as_uint(a.y);
+                    }
+                    tmem_st32(t_lane + T_ACC + c0, acc);
+                }
+                tmem_wait_st();
+            }
+            // acc += float(PV) (attention.cpp:330-333)
             mbar_wait(&sm.pv_full, bi & 1);
             tc_fence_after();
 #pragma unroll
@@ -471,11 +571,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (bi > 0) tmem_ld32(t_lane + T_ACC + c0, acc);
                 tmem_wait_ld();
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float pf = __int2float_rn(static_cast<int32_t>(pv[j]));
-                    const float a = bi > 0 ? __fadd_rn(__fmul_rn(__uint_as_float(acc[j]), alpha), pf)
-                                           : pf;
-                    acc[j] = __float_as_uint(a);
+                for (int j = 0; j < 32; j += 2) {
+                    float2 pf;
+                    if (pv_magic) {
+                        pf = fsub2(make_float2(__int_as_float(static_cast<int32_t>(pv[j]) + kMagicBits),
+                                               __int_as_float(static_cast<int32_t>(pv[j + 1]) + kMagicBits)),
+                                   f2(kMagic));
+                    } else {
+                        pf = make_float2(__int2float_rn(static_cast<int32_t>(pv[j])),
+                                         __int2float_rn(static_cast<int32_t>(pv[j + 1])));
+                    }
+                    const float2 a =
+                        bi > 0 ? fadd2(make_float2(__uint_as_float(acc[j]), __uint_as_float(acc[j + 1])), pf)
+                               : pf;
+                    acc[j] = __float_as_uint(a.x);
+                    acc[j + 1] = __float_as_uint(a.y);
                 }
                 tmem_st32(t_lane + T_ACC + c0, acc);
             }
@@ -486,8 +596,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ++bi;
         }
         // epilogue: O = (acc / l) * sV
-        mbar_wait(&sm.l_full, 0);
-        const float lr = sm.lfin[row];
         const float sv = p.sv[slice];
         tc_fence_after();
         const int64_t d = p.d;
@@ -502,7 +610,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 float out[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
-                    out[j] = __fmul_rn(__fdiv_rn(__uint_as_float(acc[j]), lr), sv);
+                    out[j] = __fmul_rn(__fdiv_rn(__uint_as_float(acc[j]), l), sv);
                 if (vec && c0 + 32 <= d) {
 #pragma unroll
                     for (int j = 0; j < 32; j += 4)
@@ -563,6 +671,23 @@ static bool make_map(CUtensorMap* map, const int8_t* base, int64_t slices, int64
     return r == CUDA_SUCCESS;
 }
 
+template <int D, bool AUDIT>
+static cudaError_t launch_k(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                            const Params& p, int64_t slices, cudaStream_t stream) {
+    const size_t smem = sizeof(Smem<D>) + 1024;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(int_flash_fwd_kernel<D, AUDIT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    dim3 grid(static_cast<unsigned>(p.q_tiles), static_cast<unsigned>(slices));
+    int_flash_fwd_kernel<D, AUDIT><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+    return cudaGetLastError();
+}
+
 template <int D>
 static cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
     CUtensorMap tq, tk, tv;
@@ -582,18 +707,8 @@ static cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
     p.flags = a.flags;
     p.extra = (a.flags & IFA_FLAG_SQRT_D) ? 1.0f / sqrtf(static_cast<float>(a.d)) : 1.0f;
     p.q_tiles = static_cast<int32_t>((a.n + BM - 1) / BM);
-    const size_t smem = sizeof(Smem<D>) + 1024;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(int_flash_fwd_kernel<D>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    dim3 grid(static_cast<unsigned>(p.q_tiles), static_cast<unsigned>(a.slices));
-    int_flash_fwd_kernel<D><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
-    return cudaGetLastError();
+    if (a.audit != nullptr) return launch_k<D, true>(tq, tk, tv, p, a.slices, stream);
+    return launch_k<D, false>(tq, tk, tv, p, a.slices, stream);
 }
 
 }  // namespace attn
