@@ -285,6 +285,8 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--dist", default="normal", choices=["normal", "uniform"],
+                    help="synthetic activations: N(0,1) or U(-0.5,0.5) (eval.cpp:46-51)")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip e2e / cpu baseline / fp16 / int8-peak probes")
     args = ap.parse_args()
@@ -321,9 +323,13 @@ def main() -> None:
 
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
-    q = torch.randn((slices, N, d), generator=gen, device=dev, dtype=torch.float32)
-    k = torch.randn((slices, N, d), generator=gen, device=dev, dtype=torch.float32)
-    v = torch.randn((slices, N, d), generator=gen, device=dev, dtype=torch.float32)
+    def synth():
+        if args.dist == "uniform":
+            return torch.rand((slices, N, d), generator=gen, device=dev,
+                              dtype=torch.float32) - 0.5
+        return torch.randn((slices, N, d), generator=gen, device=dev, dtype=torch.float32)
+
+    q, k, v = synth(), synth(), synth()
     plan = AttentionPlan(slices, N, d, bc=bc, br=128, causal=causal, device=dev)
 
     stream = torch.cuda.current_stream(dev)
@@ -381,7 +387,8 @@ def main() -> None:
         "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "i8",
-        "data": "synthetic: torch.randn N(0,1) f32 Q/K/V resident in HBM (seed 1234+rank)",
+        "data": f"synthetic: {'N(0,1)' if args.dist == 'normal' else 'U(-0.5,0.5)'} f32 "
+                "Q/K/V (torch generator, seed 1234+rank) resident in HBM",
         "config": {"workload": desc, "batch": B, "heads": H, "seq_len": N, "head_dim": d,
                    "bc": bc, "causal": causal, "slices_per_rank": slices,
                    "parallelism": f"(b,h)-slice sharding x{world}, no data-path collective",

@@ -93,6 +93,12 @@ int ifa_int_flash_fwd(const int8_t* q, const float* sq, const int8_t* k, const f
 /* Writes {127, 0, 1, 0, 0} into a device ifa_pcode_audit (async on stream). */
 int ifa_audit_init(ifa_pcode_audit* audit, void* stream);
 
+/* HOST pointer out128[0..127]: the exact decision boundaries the kernel uses
+ * to settle ambiguous weight codes, B[k] = smallest float x with
+ * (int)roundf(127*expf(x)) >= k+1 (k < 127), out128[127] = +inf.  Exposed so
+ * tests can check them against an exhaustive scan of the reference's libm. */
+int ifa_code_bounds(float* out128);
+
 /* Message of the last failing call on this host thread ("" if none). */
 const char* ifa_last_error(void);
 

@@ -517,3 +517,73 @@ uint64_t ifa_or_fnv1a64(const void *data, int64_t nbytes) {
     }
     return h;
 }
+
+/* ------------------------------------------------------------------ */
+/* Decision boundaries of the weight code (attention.cpp:306-307)       */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    uint32_t lo, hi; /* bit-pattern range [lo, hi) of negative floats */
+    int first_code, last_code, monotone;
+    float bounds[127];
+    int have[127];
+} code_scan;
+
+static void *code_scan_worker(void *arg) {
+    code_scan *cs = (code_scan *)arg;
+    int prev = -1;
+    cs->monotone = 1;
+    for (int k = 0; k < 127; ++k) cs->have[k] = 0;
+    /* walk x upwards: bit patterns of negative floats decrease as x grows */
+    for (uint32_t b = cs->hi; b-- > cs->lo;) {
+        float x;
+        memcpy(&x, &b, 4);
+        const int code = (int)roundf(127.0f * expf(x));
+        if (prev >= 0) {
+            if (code < prev) cs->monotone = 0;
+            for (int k = prev; k < code; ++k) { /* crossed boundary k -> k+1 */
+                cs->bounds[k] = x;
+                cs->have[k] = 1;
+            }
+        } else {
+            cs->first_code = code;
+        }
+        prev = code;
+    }
+    cs->last_code = prev;
+    return NULL;
+}
+
+int ifa_or_code_bounds_exhaustive(float *out, int threads) {
+    const uint32_t lo = 0x80000000u, hi = 0xC2D00001u; /* -0 .. -104 inclusive */
+    if (threads < 1) threads = 1;
+    if (threads > 64) threads = 64;
+    code_scan *cs = (code_scan *)calloc((size_t)threads, sizeof(code_scan));
+    pthread_t tid[64];
+    const uint32_t span = (hi - lo + (uint32_t)threads - 1) / (uint32_t)threads;
+    for (int t = 0; t < threads; ++t) {
+        cs[t].lo = lo + (uint32_t)t * span;
+        cs[t].hi = cs[t].lo + span < hi ? cs[t].lo + span : hi;
+        pthread_create(&tid[t], NULL, code_scan_worker, &cs[t]);
+    }
+    for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+    /* chunk t covers larger (more negative) x for larger t; stitch from the
+     * most negative chunk upwards */
+    int mono = 1, prev = -1;
+    for (int k = 0; k < 127; ++k) out[k] = 0.0f;
+    for (int t = threads - 1; t >= 0; --t) {
+        if (!cs[t].monotone) mono = 0;
+        if (prev >= 0) {
+            if (cs[t].first_code < prev) mono = 0;
+            /* boundary crossed exactly at this chunk's first (most negative) x */
+            float x0;
+            uint32_t b0 = cs[t].hi - 1;
+            memcpy(&x0, &b0, 4);
+            for (int k = prev; k < cs[t].first_code; ++k) out[k] = x0;
+        }
+        for (int k = 0; k < 127; ++k)
+            if (cs[t].have[k]) out[k] = cs[t].bounds[k];
+        prev = cs[t].last_code;
+    }
+    free(cs);
+    return mono;
+}

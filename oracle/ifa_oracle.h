@@ -85,6 +85,12 @@ int ifa_or_reference_attention(const float *q, const float *k, const float *v, i
 void ifa_or_error_accum(const float *reference, const float *candidate, int64_t count,
                         double *num, double *den);
 
+/* Exhaustive scan of code(x) = (int)roundf(127*expf(x)) over every float in
+ * [-104, 0] (libm expf, as the reference): writes B[k] = smallest x with
+ * code(x) >= k+1 (k = 0..126) into out[0..126] and returns 1 if code is
+ * non-decreasing in x, 0 otherwise.  Uses `threads` host threads. */
+int ifa_or_code_bounds_exhaustive(float *out, int threads);
+
 /* FNV-1a-64 over raw bytes (SURVEY.md Appendix A hash recipe). */
 uint64_t ifa_or_fnv1a64(const void *data, int64_t nbytes);
 

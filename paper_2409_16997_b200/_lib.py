@@ -26,6 +26,7 @@ EXPORTED_SYMBOLS = (
     "ifa_quantize_per_tensor",
     "ifa_int_flash_fwd",
     "ifa_audit_init",
+    "ifa_code_bounds",
     "ifa_last_error",
     "ifa_version",
 )
@@ -69,6 +70,8 @@ def load() -> C.CDLL:
     lib.ifa_int_flash_fwd.restype = C.c_int
     lib.ifa_audit_init.argtypes = [vp, vp]
     lib.ifa_audit_init.restype = C.c_int
+    lib.ifa_code_bounds.argtypes = [vp]
+    lib.ifa_code_bounds.restype = C.c_int
     lib.ifa_last_error.argtypes = []
     lib.ifa_last_error.restype = C.c_char_p
     lib.ifa_version.argtypes = []

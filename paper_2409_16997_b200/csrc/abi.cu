@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <string>
 
+#include "code_bounds.h"
 #include "ifa_internal.h"
 
 namespace {
@@ -50,6 +51,14 @@ __global__ void audit_init_kernel(ifa_pcode_audit* a) {
 extern "C" {
 
 const char* ifa_last_error(void) { return g_err.c_str(); }
+
+int ifa_code_bounds(float* out128) {
+    g_err.clear();
+    if (!out128) return fail(IFA_EINVAL, "ifa_code_bounds: null pointer");
+    const float* b = ifa_b200::code_bounds();
+    for (int k = 0; k < 128; ++k) out128[k] = b[k];
+    return IFA_OK;
+}
 
 const char* ifa_version(void) { return "ifa_b200 0.1 sm_100a (tcgen05 kind::i8)"; }
 

@@ -13,26 +13,27 @@
 // plus the PCodeAudit bookkeeping (:309-311, :319-326, :343-355) and the
 // causal extension (keys j <= row i only).
 //
-// One CTA owns a 128-row Q tile of one (b,h) slice.  Warp roles (16 warps):
+// One CTA owns a 128-row Q tile of one (b,h) slice.  Warp roles (22 warps):
 //   warp 0       TMA producer: Q once, then a STAGES-deep ring of K / V tiles
 //                (128 keys x D int8, 128B/64B swizzle) + the K scales.
-//   warp 1       MMA issuer (one thread): S = Q.K^T (tcgen05.mma kind::i8,
-//                A and B from SMEM) into TMEM; PV = P.V (A = P from TMEM,
-//                B = V from SMEM, MN-major) into TMEM.
-//   warp 2       TMEM allocator.
-//   warps 4-11   softmax: two threads per Q row (TMEM lane), each owning 64
-//                of the 128 key columns; tcgen05.ld the int32 S half-row,
-//                dequantize, exchange the half-row max through SMEM, exact
-//                requantization of P (MUFU estimate + rounding guard, exact
-//                glibc-expf fallback), tcgen05.st the packed int8 codes.
-//   warps 12-15  correction: acc = acc*alpha + float(PV) on the f32
-//                accumulator kept in TMEM, l = l*alpha + sum(P); final
-//                O = (acc/l)*sV epilogue.
+//   warp 1       TMEM allocator + MMA issuer (one thread): S = Q.K^T
+//                (tcgen05.mma kind::i8, A and B from SMEM) into TMEM;
+//                PV = P.V (A = P from TMEM, B = V from SMEM, MN-major) plus
+//                P.1 (a 16-column all-ones B tile: the exact int32 row sum
+//                of the codes) into TMEM.
+//   warps 2-17   softmax: four threads per Q row (TMEM lane), each owning 32
+//                of the 128 key columns; tcgen05.ld the int32 S slice,
+//                dequantize, exchange the partial row max through SMEM,
+//                exact requantization of P (MUFU estimate + rounding guard,
+//                exact glibc-expf fallback), tcgen05.st the packed codes.
+//   warps 18-21  correction: acc = acc*alpha + float(PV) on the f32
+//                accumulator kept in TMEM, l = l*alpha + float(rowsum P);
+//                final O = (acc/l)*sV epilogue.
 // Elementwise math uses sm_100 packed FADD2/FMUL2/FFMA2 (IEEE RN per lane,
 // bit-identical to the scalar ops) and magic-number int<->float conversion
 // so the XU (conversion/MUFU) pipe only carries the EX2.
-// TMEM columns: S [0,128) | PV [128,256) | ACC [256,384) | P0 [384,416) |
-// P1 [416,448).
+// TMEM columns: S [0,128) | PV [128,128+D) + rowsum [128+D,144+D) |
+// ACC [272,272+D) | P0 [400,432) | P1 [432,464).
 //
 // Bc (the reference's KV block size, which changes results) is honoured:
 // a block of <= 128 keys is one pipeline item; a larger block is processed
@@ -44,6 +45,7 @@
 
 #include <cstdint>
 
+#include "code_bounds.h"
 #include "exact_expf.cuh"
 #include "ifa_internal.h"
 #include "ptx.cuh"
@@ -57,18 +59,28 @@ namespace attn {
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int STAGES = 3;
-constexpr int NUM_THREADS = 512;
+constexpr int SPLIT = 4;                 // softmax threads per Q row
+constexpr int NCOL = BN / SPLIT;         // key columns per softmax thread
+constexpr int SOFT_WARP0 = 2;
+constexpr int SOFT_WARPS = 4 * SPLIT;    // softmax warps (4 lane quarters x SPLIT)
+constexpr int CORR_WARP0 = SOFT_WARP0 + SOFT_WARPS;
+constexpr int NUM_THREADS = 32 * (CORR_WARP0 + 4);
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t T_S = 0, T_PV = 128, T_ACC = 256, T_P0 = 384;
+constexpr uint32_t T_S = 0, T_PV = 128, T_ACC = 272, T_P0 = 400;
 constexpr float kMagic = 12582912.0f;       // 1.5 * 2^23: float(i) = bits(i + M) - M
 constexpr int32_t kMagicBits = 0x4B400000;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLog2_127 = 6.9886846867721655f;
-// MUFU estimate of y = 127*e^x is within 1.6e-4 of fl(127*fl(expf(x)))
-// (|t| <= 7 rounding 2^-22 + log2e/log2(127) constants 2^-22 + ex2.approx
-// 2^-21 relative); codes whose estimate lies within kGuard of a rounding
-// boundary are recomputed exactly.
-constexpr float kGuardThresh = 0.5f - 2.5e-4f;
+// The fast estimate y = ex2(s*log2e + c_r), c_r = log2(127) - m*log2e, is
+// within  kGuardBase + kGuardScale * (|m*log2e| + |c_r|)  of the reference's
+// fl(127*fl(expf(fl(s - m)))): in t, half an ulp of |t| < 8, of m*log2e and
+// of c_r, the float log2e / log2(127) constants; then ex2.approx (2^-22.5
+// rel) and the reference's own two roundings; times 127*ln2.  Measured
+// maxima (tools/microbench/guard.cu, 2^28 points per m) stay below half of
+// this bound.  Codes whose estimate lies within that band of a rounding
+// boundary (a half-integer) are settled exactly (code_bounds.h).
+constexpr float kGuardBase = 1.3e-4f;
+constexpr float kGuardScale = 5.5e-6f;
 
 enum ItemKind : uint32_t {
     K_MAXONLY = 1u,   // pass-1 sub-tile of a multi-tile block: contributes to the row max
@@ -80,46 +92,49 @@ enum ItemKind : uint32_t {
 };
 
 struct Item {
-    int64_t key0;
+    int32_t key0;
     int32_t width;
     uint32_t kind;
 };
 
-// Deterministic item sequence shared by every warp role.
+// Deterministic item sequence shared by every warp role (n < 2^31).
 struct ItemGen {
-    int64_t n, bc, kv_limit;
-    int64_t b0 = 0;
+    int32_t n, bc, kv_limit;
+    int32_t b0 = 0;
     int32_t s = 0, pass = 0;
 
-    __device__ ItemGen(int64_t n_, int64_t bc_, int64_t kv_limit_)
+    __device__ ItemGen(int32_t n_, int32_t bc_, int32_t kv_limit_)
         : n(n_), bc(bc_), kv_limit(kv_limit_) {}
 
-    __device__ bool next(Item& it) {
+    __device__ __forceinline__ bool next(Item& it) {
         if (b0 >= kv_limit) return false;
-        const int64_t blk_end = (bc >= n - b0) ? n : b0 + bc;
-        const int64_t lim_end = blk_end < kv_limit ? blk_end : kv_limit;
-        const int64_t len = lim_end - b0;
-        const int32_t nsub = static_cast<int32_t>((len + BN - 1) / BN);
-        it.key0 = b0 + static_cast<int64_t>(BN) * s;
-        const int64_t rem = lim_end - it.key0;
-        it.width = static_cast<int32_t>(rem < BN ? rem : BN);
-        if (nsub == 1) {
+        const int32_t blk_end = (bc >= n - b0) ? n : b0 + bc;
+        const int32_t lim_end = blk_end < kv_limit ? blk_end : kv_limit;
+        it.key0 = b0 + BN * s;
+        const int32_t rem = lim_end - it.key0;
+        it.width = rem < BN ? rem : BN;
+        if (lim_end - b0 <= BN) {  // one sub-tile: single pass
             it.kind = K_BEGIN | K_MAXDONE | K_PV | K_PV_FIRST | K_END;
             b0 = blk_end;
-            s = 0;
-            pass = 0;
-        } else if (pass == 0) {
-            it.kind = K_MAXONLY | (s == 0 ? K_BEGIN : 0u) | (s == nsub - 1 ? K_MAXDONE : 0u);
-            if (++s == nsub) {
+            return true;
+        }
+        const bool last = rem <= BN;
+        if (pass == 0) {
+            it.kind = K_MAXONLY | (s == 0 ? K_BEGIN : 0u) | (last ? K_MAXDONE : 0u);
+            if (last) {
                 s = 0;
                 pass = 1;
+            } else {
+                ++s;
             }
         } else {
-            it.kind = K_PV | (s == 0 ? K_PV_FIRST : 0u) | (s == nsub - 1 ? K_END : 0u);
-            if (++s == nsub) {
+            it.kind = K_PV | (s == 0 ? K_PV_FIRST : 0u) | (last ? K_END : 0u);
+            if (last) {
                 b0 = blk_end;
                 s = 0;
                 pass = 0;
+            } else {
+                ++s;
             }
         }
         return true;
@@ -128,7 +143,6 @@ struct ItemGen {
 
 struct RingEntry {
     float alpha[BM];
-    int32_t psum[2][BM];
 };
 
 template <int D>
@@ -136,8 +150,10 @@ struct alignas(1024) Smem {
     uint8_t q[BM * D];
     uint8_t k[STAGES][BN * D];
     uint8_t v[STAGES][BN * D];
+    uint8_t ones[16 * BN];  // all-ones B tile: P . 1 = exact int32 row sum of the codes
     float sk[STAGES][BN];
-    float xmax[2][2][BM];  // [item parity][half][row]: half-row max exchange
+    float xmax[2][SPLIT][BM];  // [item parity][part][row]: partial row max exchange
+    float bounds[128];         // B[k]: exact code decision boundaries (code_bounds.h)
     RingEntry ring[4];     // per-block alpha and code sums for the correction warps
     uint64_t q_full;
     uint64_t k_full[STAGES], v_full[STAGES], kv_empty[STAGES];
@@ -154,56 +170,81 @@ struct Params {
     const float* sv;
     float* o;
     ifa_pcode_audit* audit;
-    int64_t n;
-    int64_t d;
-    int64_t bc;
+    int32_t n;
+    int32_t d;
+    int32_t bc;  // clamped to n by the host (any Bc >= n is one block)
     uint32_t flags;
     float extra;  // 1/sqrt(d) when IFA_FLAG_SQRT_D, else 1
     int32_t q_tiles;
+    float bounds[128];
 };
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
-// Requantize 8 consecutive scores: packed codes (2 words) for
-// round(127*expf(s - m_new)); returns the code sum via dp4a into psum.
-__device__ __forceinline__ void codes8(const float* s, float m_new, uint32_t* w,
-                                       int32_t& psum) {
-    float x[8], r[8], df[8];
-    const float2 negm = f2(-m_new);
+// Requantize this thread's NCOL scores to the reference's codes
+// (int)round(127*expf(s - m_new)), packed 4 per word.  Fast path: y =
+// ex2(s*log2e + c_r) with c_r = log2(127) - m_new*log2e, rounded by the
+// magic-number add; every element also measures its distance to that
+// integer.  An estimate within the guard band of a rounding boundary k+1/2
+// (rare) is settled exactly by one comparison against the precomputed
+// boundary B[k] of the reference's code function (code_bounds.h).
+__device__ __forceinline__ void codes_part(const float (&s)[NCOL], float m_new, float c_r,
+                                           float thresh, const float* bounds,
+                                           uint32_t (&w)[NCOL / 4]) {
+    const float2 c2 = f2(c_r);
 #pragma unroll
-    for (int e = 0; e < 8; e += 2) {
-        const float2 xx = fadd2(make_float2(s[e], s[e + 1]), negm);
-        const float2 t = ffma2(xx, f2(kLog2e), f2(kLog2_127));
-        const float2 y = make_float2(ex2_approx(t.x), ex2_approx(t.y));
-        const float2 rr = fadd2(y, f2(kMagic));
-        const float2 rf = fsub2(rr, f2(kMagic));
-        const float2 d2 = fsub2(y, rf);
-        x[e] = xx.x;
-        x[e + 1] = xx.y;
-        r[e] = rr.x;
-        r[e + 1] = rr.y;
-        df[e] = d2.x;
-        df[e + 1] = d2.y;
-    }
-    const float g = fmaxf(fmax3(fmax3(fabsf(df[0]), fabsf(df[1]), fabsf(df[2])),
-                                fmax3(fabsf(df[3]), fabsf(df[4]), fabsf(df[5])), fabsf(df[6])),
-                          fabsf(df[7]));
-    if (g > kGuardThresh) {
+    for (int g0 = 0; g0 < NCOL; g0 += 8) {
+        float df[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-            r[e] = __int_as_float(kMagicBits + exact_code(x[e]));
+        for (int c = g0; c < g0 + 8; c += 4) {
+            const float2 ta = ffma2(make_float2(s[c], s[c + 1]), f2(kLog2e), c2);
+            const float2 tb = ffma2(make_float2(s[c + 2], s[c + 3]), f2(kLog2e), c2);
+            const float2 ya = make_float2(ex2_approx(ta.x), ex2_approx(ta.y));
+            const float2 yb = make_float2(ex2_approx(tb.x), ex2_approx(tb.y));
+            const float2 ra = fadd2(ya, f2(kMagic));  // bits: magic + nearest integer
+            const float2 rb = fadd2(yb, f2(kMagic));
+            const float2 da = fsub2(ya, fsub2(ra, f2(kMagic)));  // distance to it
+            const float2 db = fsub2(yb, fsub2(rb, f2(kMagic)));
+            df[c - g0] = da.x;
+            df[c - g0 + 1] = da.y;
+            df[c - g0 + 2] = db.x;
+            df[c - g0 + 3] = db.y;
+            w[c >> 2] = __byte_perm(__byte_perm(__float_as_uint(ra.x), __float_as_uint(ra.y), 0x0040),
+                                    __byte_perm(__float_as_uint(rb.x), __float_as_uint(rb.y), 0x0040),
+                                    0x5410);
+        }
+        const float g = fmaxf(fmax3(fmax3(fabsf(df[0]), fabsf(df[1]), fabsf(df[2])),
+                                    fmax3(fabsf(df[3]), fabsf(df[4]), fabsf(df[5])), fabsf(df[6])),
+                              fabsf(df[7]));
+        if (g > thresh) {  // rare: settle the ambiguous codes exactly
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                if (fabsf(df[e]) > thresh) {
+                    const int c = g0 + e;
+                    const uint32_t sh = 8u * (c & 3);
+                    int k = static_cast<int>((w[c >> 2] >> sh) & 0xffu) - (df[e] < 0.0f ? 1 : 0);
+                    k = k < 0 ? 0 : (k > 126 ? 126 : k);
+                    const int code = k + (__fsub_rn(s[c], m_new) >= bounds[k] ? 1 : 0);
+                    w[c >> 2] = (w[c >> 2] & ~(0xffu << sh)) | (static_cast<uint32_t>(code) << sh);
+                }
+            }
+        }
     }
-    w[0] = __byte_perm(__byte_perm(__float_as_uint(r[0]), __float_as_uint(r[1]), 0x0040),
-                       __byte_perm(__float_as_uint(r[2]), __float_as_uint(r[3]), 0x0040),
-                       0x5410);
-    w[1] = __byte_perm(__byte_perm(__float_as_uint(r[4]), __float_as_uint(r[5]), 0x0040),
-                       __byte_perm(__float_as_uint(r[6]), __float_as_uint(r[7]), 0x0040),
-                       0x5410);
-    psum = static_cast<int32_t>(__dp4a(w[0], 0x01010101u, static_cast<uint32_t>(psum)));
-    psum = static_cast<int32_t>(__dp4a(w[1], 0x01010101u, static_cast<uint32_t>(psum)));
 }
 
-template <int D, bool AUDIT>
+// Max of NCOL floats as a three-input tree.
+__device__ __forceinline__ float row_max(const float (&s)[NCOL]) {
+    static_assert(NCOL == 32, "tree below is written for 32 columns");
+    float a[11];
+#pragma unroll
+    for (int j = 0; j < 10; ++j) a[j] = fmax3(s[3 * j], s[3 * j + 1], s[3 * j + 2]);
+    a[10] = fmaxf(s[30], s[31]);
+    const float b0 = fmax3(a[0], a[1], a[2]), b1 = fmax3(a[3], a[4], a[5]);
+    const float b2 = fmax3(a[6], a[7], a[8]), b3 = fmaxf(a[9], a[10]);
+    return fmaxf(fmax3(b0, b1, b2), b3);
+}
+
+template <int D, bool AUDIT, bool EXTRA>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     int_flash_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_k,
@@ -213,11 +254,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     constexpr uint32_t kTileBytes = BN * D;
     constexpr uint32_t kIdescS = idesc_i8(BM, BN, false, false);
     constexpr uint32_t kIdescPV = idesc_i8(BM, D, false, true);
+    constexpr uint32_t kIdescSum = idesc_i8(BM, 16, false, false);
     const float kNegInf = -__int_as_float(0x7f800000);
 
-    extern __shared__ uint8_t smem_raw[];
-    Smem<D>& sm = *reinterpret_cast<Smem<D>*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    Smem<D>& sm = *reinterpret_cast<Smem<D>*>(smem_raw);
 
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
@@ -225,31 +266,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // Heavier causal tiles first (longest-processing-time order).
     const int32_t qt = causal ? (p.q_tiles - 1 - static_cast<int32_t>(blockIdx.x))
                               : static_cast<int32_t>(blockIdx.x);
-    const int64_t q0 = static_cast<int64_t>(qt) * BM;
-    const int64_t slice = blockIdx.y;
-    const int64_t n = p.n;
-    int64_t kv_limit = n;
+    const int32_t q0 = qt * BM;
+    const int32_t slice = static_cast<int32_t>(blockIdx.y);
+    const int32_t n = p.n;
+    int32_t kv_limit = n;
     if (causal && q0 + BM < kv_limit) kv_limit = q0 + BM;
 
     if (threadIdx.x == 0) {
+        if (smem_u32(smem_raw) & 1023) __trap();  // SWIZZLE_128B tiles need 1 KiB alignment
         mbar_init(&sm.q_full, 1);
         for (int i = 0; i < STAGES; ++i) {
             mbar_init(&sm.k_full[i], 32);
             mbar_init(&sm.v_full[i], 1);
-            mbar_init(&sm.kv_empty[i], 1 + 8);
+            mbar_init(&sm.kv_empty[i], 1 + SOFT_WARPS);
         }
         mbar_init(&sm.s_full, 1);
-        mbar_init(&sm.s_empty, 8);
+        mbar_init(&sm.s_empty, SOFT_WARPS);
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&sm.p_full[i], 8);
+            mbar_init(&sm.p_full[i], SOFT_WARPS);
             mbar_init(&sm.p_empty[i], 1);
         }
         mbar_init(&sm.pv_full, 1);
         mbar_init(&sm.pv_empty, 4);
-        for (int i = 0; i < 4; ++i) mbar_init(&sm.ring_full[i], 8);
+        for (int i = 0; i < 4; ++i) mbar_init(&sm.ring_full[i], 4);
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc<TMEM_COLS>(&sm.tmem_base);
+    if (threadIdx.x < 128) sm.bounds[threadIdx.x] = p.bounds[threadIdx.x];
+    if (threadIdx.x < 16 * BN / 16)
+        reinterpret_cast<uint4*>(sm.ones)[threadIdx.x] = make_uint4(0x01010101u, 0x01010101u,
+                                                                    0x01010101u, 0x01010101u);
+    fence_proxy_async_shared();  // the all-ones tile is read by the tensor core
+    if (warp == 1) tmem_alloc<TMEM_COLS>(&sm.tmem_base);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -264,10 +311,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tma_prefetch_desc(&tm_k);
             tma_prefetch_desc(&tm_v);
             mbar_arrive_expect_tx(&sm.q_full, BM * D);
-            tma_load_3d(sm.q, &tm_q, &sm.q_full, 0, static_cast<int32_t>(q0),
-                        static_cast<int32_t>(slice), pol_stream);
+            tma_load_3d(sm.q, &tm_q, &sm.q_full, 0, q0, slice, pol_stream);
         }
-        const float* sk_slice = p.sk + slice * n;
+        const float* sk_slice = p.sk + static_cast<int64_t>(slice) * n;
         ItemGen gen(n, p.bc, kv_limit);
         Item it;
         uint32_t i = 0;
@@ -275,7 +321,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t st = i % STAGES;
             if (i >= STAGES) mbar_wait(&sm.kv_empty[st], ((i / STAGES) - 1) & 1);
             float4 kv4;
-            const int64_t key = it.key0 + lane * 4;
+            const int32_t key = it.key0 + lane * 4;
             if (key + 3 < n && (reinterpret_cast<uintptr_t>(sk_slice + key) & 15) == 0) {
                 kv4 = __ldg(reinterpret_cast<const float4*>(sk_slice + key));
             } else {
@@ -287,13 +333,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             reinterpret_cast<float4*>(sm.sk[st])[lane] = kv4;
             if (lane == 0) {
                 mbar_arrive_expect_tx(&sm.k_full[st], kTileBytes);
-                tma_load_3d(sm.k[st], &tm_k, &sm.k_full[st], 0, static_cast<int32_t>(it.key0),
-                            static_cast<int32_t>(slice), pol_keep);
+                tma_load_3d(sm.k[st], &tm_k, &sm.k_full[st], 0, it.key0, slice, pol_keep);
                 if (it.kind & K_PV) {
                     mbar_arrive_expect_tx(&sm.v_full[st], kTileBytes);
-                    tma_load_3d(sm.v[st], &tm_v, &sm.v_full[st], 0,
-                                static_cast<int32_t>(it.key0), static_cast<int32_t>(slice),
-                                pol_keep);
+                    tma_load_3d(sm.v[st], &tm_v, &sm.v_full[st], 0, it.key0, slice, pol_keep);
                 } else {
                     mbar_arrive(&sm.v_full[st]);
                 }
@@ -308,6 +351,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_wait(&sm.q_full, 0);
             tc_fence_after();
             const uint32_t q_base = smem_u32(sm.q);
+            const uint32_t ones_base = smem_u32(sm.ones);
             ItemGen gen(n, p.bc, kv_limit);
             Item it;
             uint32_t i = 0, pi = 0, bi = 0;
@@ -326,6 +370,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const uint64_t bdesc = smem_desc(v_base + kk * 32 * D, 16, kSbo, kLayout);
                     const uint32_t acc = ((kind & K_PV_FIRST) && kk == 0) ? 0u : 1u;
                     mma_i8_ts(tmem + T_PV, tmem + p_col + kk * 8, bdesc, kIdescPV, acc);
+                    // P . 1 (16 identical columns): the block's exact code row sum.
+                    const uint64_t odesc = smem_desc(ones_base + kk * 32, 16, 1024, kLayoutSw128);
+                    mma_i8_ts(tmem + T_PV + D, tmem + p_col + kk * 8, odesc, kIdescSum, acc);
                 }
                 mma_commit(&sm.p_empty[pidx & 1]);
                 mma_commit(&sm.kv_empty[st]);
@@ -364,21 +411,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (have_prev) issue_pv(prev_st, prev_ph, prev_kind, prev_pi);
         }
         __syncwarp();
-    } else if (warp >= 4 && warp < 12) {
+    } else if (warp < CORR_WARP0) {
         // ------------------------------------------------------------ softmax
         const uint32_t quarter = warp & 3;
-        const uint32_t half = (warp - 4) >> 2;
+        const uint32_t part = (warp - SOFT_WARP0) >> 2;  // which NCOL-column slice of the row
         const int32_t row = static_cast<int32_t>(quarter * 32 + lane);
-        const int64_t grow = q0 + row;
+        const int32_t grow = q0 + row;
         const bool row_ok = grow < n;
-        const float sq_r = row_ok ? p.sq[slice * n + grow] : 0.0f;
-        const uint32_t t_lane = tmem + ((quarter * 32) << 16);
-        const uint32_t c_base = 64 * half;  // first key column owned by this thread
+        const float sq_r = row_ok ? p.sq[static_cast<int64_t>(slice) * n + grow] : 0.0f;
+        const uint32_t t_s = tmem + ((quarter * 32) << 16) + T_S + NCOL * part;
+        const uint32_t t_p = tmem + ((quarter * 32) << 16) + T_P0 + (NCOL / 4) * part;
+        const int32_t c_base = NCOL * part;  // first key column owned by this thread
         const uint32_t bar_id = 1 + quarter;
         const float extra = p.extra;
+        float* const xmax_mine = &sm.xmax[0][part][row];
         float m = kNegInf;
-        float blk_max = kNegInf, m_new = kNegInf, alpha = 0.0f;
-        int32_t p_sum = 0;
+        float blk_max = kNegInf, m_new = kNegInf;
         bool has_full = false, row_hit = false;
         int32_t cmin = 127, cmax = 0;
         ItemGen gen(n, p.bc, kv_limit);
@@ -388,9 +436,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t st = i % STAGES;
             mbar_wait(&sm.s_full, i & 1);
             tc_fence_after();
-            uint32_t sr[64];
-            tmem_ld32(t_lane + T_S + c_base, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-            tmem_ld32(t_lane + T_S + c_base + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+            uint32_t sr[NCOL];
+            tmem_ld32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
@@ -399,29 +446,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_wait(&sm.k_full[st], (i / STAGES) & 1);
             int32_t lim = it.width;
             if (causal) {
-                const int64_t vis = grow - it.key0 + 1;
-                if (vis < lim) lim = vis < 0 ? 0 : static_cast<int32_t>(vis);
+                const int32_t vis = grow - it.key0 + 1;
+                if (vis < lim) lim = vis < 0 ? 0 : vis;
             }
-            lim -= static_cast<int32_t>(c_base);  // columns of this half still visible
+            lim -= c_base;  // columns of this slice still visible
             // dequantize: s = float(S) * (sQ * sK) [* extra], product of scales first
-            float s[64];
-            float m_loc = kNegInf, s_min = -kNegInf;
+            float s[NCOL];
             const float4* sk4 = reinterpret_cast<const float4*>(sm.sk[st] + c_base);
 #pragma unroll
-            for (int c4 = 0; c4 < 16; ++c4) {
+            for (int c4 = 0; c4 < NCOL / 4; ++c4) {
                 const float4 k4 = sk4[c4];
                 const int c = c4 * 4;
-                const float2 sf01 = fsub2(
-                    make_float2(__int_as_float(static_cast<int32_t>(sr[c]) + kMagicBits),
-                                __int_as_float(static_cast<int32_t>(sr[c + 1]) + kMagicBits)),
-                    f2(kMagic));
-                const float2 sf23 = fsub2(
-                    make_float2(__int_as_float(static_cast<int32_t>(sr[c + 2]) + kMagicBits),
-                                __int_as_float(static_cast<int32_t>(sr[c + 3]) + kMagicBits)),
-                    f2(kMagic));
+                // float(S) exact (|S| < 2^24)
+                const float2 sf01 = make_float2(__int2float_rn(static_cast<int32_t>(sr[c])),
+                                                __int2float_rn(static_cast<int32_t>(sr[c + 1])));
+                const float2 sf23 = make_float2(__int2float_rn(static_cast<int32_t>(sr[c + 2])),
+                                                __int2float_rn(static_cast<int32_t>(sr[c + 3])));
                 float2 s01 = fmul2(sf01, fmul2(f2(sq_r), make_float2(k4.x, k4.y)));
                 float2 s23 = fmul2(sf23, fmul2(f2(sq_r), make_float2(k4.z, k4.w)));
-                if (extra != 1.0f) {
+                if (EXTRA) {
                     s01 = fmul2(s01, f2(extra));
                     s23 = fmul2(s23, f2(extra));
                 }
@@ -430,80 +473,85 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 s[c + 2] = s23.x;
                 s[c + 3] = s23.y;
             }
-            if (lim < 64) {
-#pragma unroll
-                for (int c = 0; c < 64; ++c) s[c] = c < lim ? s[c] : kNegInf;
-            }
-#pragma unroll
-            for (int c = 0; c < 64; c += 4) m_loc = fmax3(m_loc, fmax3(s[c], s[c + 1], s[c + 2]), s[c + 3]);
-            if (AUDIT) {
-#pragma unroll
-                for (int c = 0; c < 64; ++c)
-                    if (c < lim) s_min = fminf(s_min, s[c]);
-            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.kv_empty[st]);
-            // half-row max exchange with the partner thread (other half, same row)
-            sm.xmax[i & 1][half][row] = m_loc;
-            named_bar_sync(bar_id, 64);
-            m_loc = fmaxf(m_loc, sm.xmax[i & 1][half ^ 1][row]);
+            if (lim < NCOL) {
+#pragma unroll
+                for (int c = 0; c < NCOL; ++c) s[c] = c < lim ? s[c] : kNegInf;
+            }
+            float m_loc = row_max(s);
+            float s_min = -kNegInf;
+            if (AUDIT) {
+#pragma unroll
+                for (int c = 0; c < NCOL; ++c)
+                    if (c < lim) s_min = fminf(s_min, s[c]);
+            }
+            // partial row max exchange among the SPLIT threads of this row
+            xmax_mine[(i & 1) * SPLIT * BM] = m_loc;
+            named_bar_sync(bar_id, 32 * SPLIT);
+            {
+                const float* xr = &sm.xmax[i & 1][0][row];
+                m_loc = fmaxf(fmax3(xr[0], xr[BM], xr[2 * BM]), xr[3 * BM]);
+            }
 
             if (it.kind & K_BEGIN) blk_max = kNegInf;
             if (!(it.kind & K_PV) || (it.kind & K_BEGIN)) blk_max = fmaxf(blk_max, m_loc);
             if (it.kind & K_MAXDONE) {
                 m_new = (m < blk_max) ? blk_max : m;  // std::max(m, m_loc)
-                alpha = exact_expf(__fsub_rn(m, m_new));
-                p_sum = 0;
                 // the block's largest code comes from its largest score
-                has_full = blk_max != kNegInf && guarded_code(__fsub_rn(blk_max, m_new)) == 127;
+                if (AUDIT)
+                    has_full = blk_max != kNegInf &&
+                               guarded_code(__fsub_rn(blk_max, m_new)) == 127;
             }
             if (it.kind & K_PV) {
+                if ((it.kind & K_END) && part == 0) {
+                    // alpha = expf(m - m_new) (attention.cpp:298) for the correction warps
+                    sm.ring[bi & 3].alpha[row] = exact_expf(__fsub_rn(m, m_new));
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&sm.ring_full[bi & 3]);
+                }
                 if (pi >= 2) {
                     mbar_wait(&sm.p_empty[pi & 1], ((pi - 2) >> 1) & 1);
                     tc_fence_after();
                 }
-                uint32_t w[16];
-                int32_t ps = 0;
-#pragma unroll
-                for (int g = 0; g < 8; ++g) codes8(&s[8 * g], m_new, &w[2 * g], ps);
-                p_sum += ps;
-                tmem_st16(t_lane + T_P0 + 32 * (pi & 1) + 16 * half, w);
+                uint32_t w[NCOL / 4];
+                const float mL = __fmul_rn(m_new, kLog2e);
+                const float c_r = __fsub_rn(kLog2_127, mL);
+                const float thresh =
+                    0.5f - (kGuardBase + kGuardScale * (fabsf(mL) + fabsf(c_r)));
+                codes_part(s, m_new, c_r, thresh, sm.bounds, w);
+                asm volatile(
+                    "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                        t_p + 32 * (pi & 1)),
+                    "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]),
+                    "r"(w[7])
+                    : "memory");
                 if (AUDIT && row_ok && lim > 0) {
-                    float my_max = kNegInf;
-#pragma unroll
-                    for (int c = 0; c < 64; c += 4)
-                        my_max = fmax3(my_max, fmax3(s[c], s[c + 1], s[c + 2]), s[c + 3]);
-                    cmax = max(cmax, guarded_code(__fsub_rn(my_max, m_new)));
+                    cmax = max(cmax, guarded_code(__fsub_rn(row_max(s), m_new)));
                     cmin = min(cmin, guarded_code(__fsub_rn(s_min, m_new)));
                 }
                 if (it.kind & K_END) {
-                    RingEntry& re = sm.ring[bi & 3];
-                    if (half == 0) re.alpha[row] = alpha;
-                    re.psum[half][row] = p_sum;
                     if (m_new > m)
                         row_hit = has_full;
                     else if (blk_max == m_new && has_full)
                         row_hit = true;
                     m = m_new;
+                    ++bi;
                 }
                 tmem_wait_st();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&sm.p_full[pi & 1]);
-                    if (it.kind & K_END) mbar_arrive(&sm.ring_full[bi & 3]);
-                }
-                if (it.kind & K_END) ++bi;
+                if (lane == 0) mbar_arrive(&sm.p_full[pi & 1]);
                 ++pi;
             }
             ++i;
         }
         if (AUDIT && p.audit != nullptr) {
-            // rows >= n never emitted a code; the half-1 thread reports codes only
+            // rows >= n never emitted a code; only part 0 reports row facts
             int32_t my_min = row_ok ? cmin : 127;
             int32_t my_max = row_ok ? cmax : 0;
-            int32_t my_hit = (row_ok && half == 0) ? (row_hit ? 1 : 0) : 1;
-            int32_t my_rows = (row_ok && half == 0) ? 1 : 0;
+            int32_t my_hit = (row_ok && part == 0) ? (row_hit ? 1 : 0) : 1;
+            int32_t my_rows = (row_ok && part == 0) ? 1 : 0;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 my_min = min(my_min, __shfl_xor_sync(0xffffffffu, my_min, o));
@@ -520,11 +568,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                               static_cast<unsigned long long>(my_rows));
             }
         }
-    } else if (warp >= 12) {
+    } else {
         // ------------------------------------------------------------ correction
         const uint32_t quarter = warp & 3;
         const int32_t row = static_cast<int32_t>(quarter * 32 + lane);
-        const int64_t grow = q0 + row;
+        const int32_t grow = q0 + row;
         const uint32_t t_lane = tmem + ((quarter * 32) << 16);
         // P.V int32 of one block fits the magic conversion while |pv| < 2^22
         const bool pv_magic = p.bc <= 256;
@@ -535,43 +583,48 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         while (gen.next(it)) {
             if (!(it.kind & K_END)) continue;
             mbar_wait(&sm.ring_full[bi & 3], (bi >> 2) & 1);
-            const RingEntry& re = sm.ring[bi & 3];
-            const float alpha = re.alpha[row];
-            const int32_t psum = re.psum[0][row] + re.psum[1][row];
-            l = __fadd_rn(__fmul_rn(l, alpha), static_cast<float>(psum));
+            const float alpha = sm.ring[bi & 3].alpha[row];
             // acc *= alpha (attention.cpp:316-318) -- its own TMEM round trip so
             // the product is rounded before the add (ptxas contracts adjacent
             // mul.rn.f32x2/add.rn.f32x2 into FFMA2); skipped when alpha == 1
             // for the whole warp, which leaves acc bit-identical.
             if (bi > 0 && !__all_sync(0xffffffffu, alpha == 1.0f)) {
 #pragma unroll
-                for (int c0 = 0; c0 < D; c0 += 32) {
-                    uint32_t acc[32];
-                    tmem_ld32(t_lane + T_ACC + c0, acc);
+                for (int c0 = 0; c0 < D; c0 += 16) {
+                    uint32_t acc[16];
+                    tmem_ld16(t_lane + T_ACC + c0, acc);
                     tmem_wait_ld();
 #pragma unroll
-                    for (int j = 0; j < 32; j += 2) {
+                    for (int j = 0; j < 16; j += 2) {
                         const float2 a = fmul2(make_float2(__uint_as_float(acc[j]),
                                                            __uint_as_float(acc[j + 1])),
                                                f2(alpha));
                         acc[j] = __float_as_uint(a.x);
                         acc[j + 1] = __float_as_uint(a.y);
                     }
-                    tmem_st32(t_lane + T_ACC + c0, acc);
+                    tmem_st16(t_lane + T_ACC + c0, acc);
                 }
                 tmem_wait_st();
             }
-            // acc += float(PV) (attention.cpp:330-333)
+            // acc += float(PV) (attention.cpp:330-333); l = l*alpha + float(sum P)
             mbar_wait(&sm.pv_full, bi & 1);
             tc_fence_after();
+            {
+                uint32_t rs;
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
+                             : "=r"(rs)
+                             : "r"(t_lane + T_PV + D));
+                tmem_wait_ld();
+                l = __fadd_rn(__fmul_rn(l, alpha), static_cast<float>(static_cast<int32_t>(rs)));
+            }
 #pragma unroll
-            for (int c0 = 0; c0 < D; c0 += 32) {
-                uint32_t pv[32], acc[32];
-                tmem_ld32(t_lane + T_PV + c0, pv);
-                if (bi > 0) tmem_ld32(t_lane + T_ACC + c0, acc);
+            for (int c0 = 0; c0 < D; c0 += 16) {
+                uint32_t pv[16], acc[16];
+                tmem_ld16(t_lane + T_PV + c0, pv);
+                if (bi > 0) tmem_ld16(t_lane + T_ACC + c0, acc);
                 tmem_wait_ld();
 #pragma unroll
-                for (int j = 0; j < 32; j += 2) {
+                for (int j = 0; j < 16; j += 2) {
                     float2 pf;
                     if (pv_magic) {
                         pf = fsub2(make_float2(__int_as_float(static_cast<int32_t>(pv[j]) + kMagicBits),
@@ -587,7 +640,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     acc[j] = __float_as_uint(a.x);
                     acc[j + 1] = __float_as_uint(a.y);
                 }
-                tmem_st32(t_lane + T_ACC + c0, acc);
+                tmem_st16(t_lane + T_ACC + c0, acc);
             }
             tmem_wait_st();
             tc_fence_before();
@@ -598,8 +651,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // epilogue: O = (acc / l) * sV
         const float sv = p.sv[slice];
         tc_fence_after();
-        const int64_t d = p.d;
-        float* orow = p.o + (slice * n + grow) * d;
+        const int32_t d = p.d;
+        float* orow = p.o + (static_cast<int64_t>(slice) * n + grow) * d;
         const bool vec = (d % 4 == 0);
 #pragma unroll
         for (int c0 = 0; c0 < D; c0 += 32) {
@@ -627,7 +680,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     tc_fence_before();
     __syncthreads();
-    if (warp == 2) {
+    if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<TMEM_COLS>(tmem);
     }
@@ -671,20 +724,20 @@ static bool make_map(CUtensorMap* map, const int8_t* base, int64_t slices, int64
     return r == CUDA_SUCCESS;
 }
 
-template <int D, bool AUDIT>
+template <int D, bool AUDIT, bool EXTRA>
 static cudaError_t launch_k(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                             const Params& p, int64_t slices, cudaStream_t stream) {
     const size_t smem = sizeof(Smem<D>) + 1024;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(int_flash_fwd_kernel<D, AUDIT>,
+        cudaError_t e = cudaFuncSetAttribute(int_flash_fwd_kernel<D, AUDIT, EXTRA>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
         configured = true;
     }
     dim3 grid(static_cast<unsigned>(p.q_tiles), static_cast<unsigned>(slices));
-    int_flash_fwd_kernel<D, AUDIT><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+    int_flash_fwd_kernel<D, AUDIT, EXTRA><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
     return cudaGetLastError();
 }
 
@@ -701,20 +754,26 @@ static cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
     p.sv = a.sv;
     p.o = a.o;
     p.audit = a.audit;
-    p.n = a.n;
-    p.d = a.d;
-    p.bc = a.bc;
+    p.n = static_cast<int32_t>(a.n);
+    p.d = static_cast<int32_t>(a.d);
+    p.bc = static_cast<int32_t>(a.bc < a.n ? a.bc : a.n);
     p.flags = a.flags;
     p.extra = (a.flags & IFA_FLAG_SQRT_D) ? 1.0f / sqrtf(static_cast<float>(a.d)) : 1.0f;
     p.q_tiles = static_cast<int32_t>((a.n + BM - 1) / BM);
-    if (a.audit != nullptr) return launch_k<D, true>(tq, tk, tv, p, a.slices, stream);
-    return launch_k<D, false>(tq, tk, tv, p, a.slices, stream);
+    const float* bounds = code_bounds();
+    for (int k = 0; k < 128; ++k) p.bounds[k] = bounds[k];
+    const bool extra = (a.flags & IFA_FLAG_SQRT_D) != 0;
+    if (a.audit != nullptr)
+        return extra ? launch_k<D, true, true>(tq, tk, tv, p, a.slices, stream)
+                     : launch_k<D, true, false>(tq, tk, tv, p, a.slices, stream);
+    return extra ? launch_k<D, false, true>(tq, tk, tv, p, a.slices, stream)
+                 : launch_k<D, false, false>(tq, tk, tv, p, a.slices, stream);
 }
 
 }  // namespace attn
 
 cudaError_t launch_int_flash_fwd(const AttnArgs& a, cudaStream_t stream) {
-    if (a.slices > 65535) return cudaErrorInvalidValue;
+    if (a.slices > 65535 || a.n > (int64_t{1} << 30)) return cudaErrorInvalidValue;
     if (a.d <= 64) return attn::launch_d<64>(a, stream);
     return attn::launch_d<128>(a, stream);
 }
