@@ -313,9 +313,9 @@ def main() -> None:
     B, H, N, d, causal, bc, scaling, desc = WORKLOADS[args.workload]
     total_slices = B * H
     if scaling == "strong":
-        per = (total_slices + world - 1) // world
-        lo, hi = rank * per, min(total_slices, (rank + 1) * per)
-        slices = hi - lo
+        from paper_2409_16997_b200.sharding import shard_range
+        lo, hi = shard_range(total_slices, world, rank)
+        slices = max(hi - lo, 1)
         job_slices = total_slices
     else:
         slices = total_slices
