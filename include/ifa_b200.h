@@ -11,6 +11,11 @@
  *   ifa_int_flash_fwd         replaces ifa::int_flash_attention
  *                             (include/ifa/attention.hpp:85-87,
  *                             src/attention.cpp:235-357), batched over slices
+ *   ifa_*_host                the same three entry points with HOST buffers and
+ *                             the reference's synchronous calling convention
+ *                             (copies + kernels + copies on one stream, then a
+ *                             synchronize) -- what a CPU caller such as
+ *                             eval.cpp:98-102 or the verify hook binds
  *   ifa_last_error            replaces the what() of the C++ exceptions the
  *                             reference throws (std::invalid_argument /
  *                             std::overflow_error)
@@ -89,6 +94,26 @@ int ifa_int_flash_fwd(const int8_t* q, const float* sq, const int8_t* k, const f
                       const int8_t* v, const float* sv, float* o, int64_t slices, int64_t n,
                       int64_t d, int64_t br, int64_t bc, uint32_t flags,
                       ifa_pcode_audit* audit, void* stream);
+
+/* ---- host-buffer forms (drop-in for synchronous CPU callers) -------------
+ * Same arguments as above, but every array is HOST memory (pageable or
+ * pinned) and the call returns after the results are back on the host.
+ * Device memory comes from a per-thread grow-only workspace.  The quantizers
+ * reject non-finite input like require_finite (quant.cpp:14-22): IFA_EINVAL,
+ * message "<fn>: non-finite input at index <i>", *nonfinite_index = i (or
+ * INT64_MAX); codes/scales are still written.  ifa_int_flash_fwd_host also
+ * rejects sv[s] < 0 or non-finite ("quantized attention inputs: bad v
+ * scale", attention.cpp:229-231) and, when `audit` (HOST) is non-NULL,
+ * initialises it to {127, 0, 1, 0, 0} itself. */
+int ifa_quantize_per_row_host(const float* x, int64_t rows, int64_t cols, int8_t* codes,
+                              float* scales, int64_t* nonfinite_index, void* stream);
+int ifa_quantize_per_tensor_host(const float* x, int64_t slices, int64_t rows, int64_t cols,
+                                 int8_t* codes, float* slice_scales, int64_t* nonfinite_index,
+                                 void* stream);
+int ifa_int_flash_fwd_host(const int8_t* q, const float* sq, const int8_t* k, const float* sk,
+                           const int8_t* v, const float* sv, float* o, int64_t slices,
+                           int64_t n, int64_t d, int64_t br, int64_t bc, uint32_t flags,
+                           ifa_pcode_audit* audit, void* stream);
 
 /* Writes {127, 0, 1, 0, 0} into a device ifa_pcode_audit (async on stream). */
 int ifa_audit_init(ifa_pcode_audit* audit, void* stream);

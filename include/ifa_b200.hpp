@@ -1,0 +1,82 @@
+// ifa_b200.hpp -- header-only C++ shim that gives the reference's own types
+// and signatures to the B200 C-ABI (ifa_b200.h).
+//
+// Compile it together with the reference's headers (proj/include on the
+// include path) and link libifa_b200.so.  Each function here has exactly the
+// signature of the reference function it replaces, so it drops into every
+// caller SURVEY.md §8(b) b2 lists -- in particular into the reference's
+// plugin hook
+//
+//     ifa::VerifyOptions opts;                       // verify.hpp:18-24
+//     opts.int_flash = ifa_gpu::int_flash_attention; // IntFlashFn, verify.hpp:15-16
+//     ifa::run_verification(opts);                   // verify.cpp:418-450
+//
+// Errors come back as the reference's exception types: std::invalid_argument
+// for IFA_EINVAL (attention.cpp:213-233, gemm.cpp:16-20, quant.cpp:14-22),
+// std::overflow_error for IFA_EOVERFLOW (gemm.cpp:22-28), std::runtime_error
+// for IFA_ENOTSUP / IFA_ECUDA (no CPU fallback exists).
+#pragma once
+
+#include <stdexcept>
+#include <string>
+
+#include "ifa/attention.hpp"
+#include "ifa/quant.hpp"
+#include "ifa_b200.h"
+
+namespace ifa_gpu {
+
+inline void check(int rc) {
+    if (rc == IFA_OK) return;
+    const std::string msg = ifa_last_error();
+    if (rc == IFA_EINVAL) throw std::invalid_argument(msg);
+    if (rc == IFA_EOVERFLOW) throw std::overflow_error(msg);
+    throw std::runtime_error("ifa_b200 (" + std::to_string(rc) + "): " + msg);
+}
+
+/// Drop-in for ifa::quantize_per_row (quant.hpp:30, quant.cpp:44-57).
+inline ifa::QuantizedRows quantize_per_row(const ifa::FloatMatrix& m) {
+    ifa::QuantizedRows out{ifa::Int8Matrix(m.rows(), m.cols()), ifa::ScaleVector(m.rows())};
+    check(ifa_quantize_per_row_host(m.data(), m.rows(), m.cols(), out.values.data(),
+                                    out.scales.data(), nullptr, nullptr));
+    return out;
+}
+
+/// Drop-in for ifa::quantize_per_tensor (quant.hpp:33, quant.cpp:59-69).
+inline ifa::QuantizedTensor quantize_per_tensor(const ifa::FloatMatrix& m) {
+    ifa::QuantizedTensor out{ifa::Int8Matrix(m.rows(), m.cols()), 0.0f};
+    check(ifa_quantize_per_tensor_host(m.data(), 1, m.rows(), m.cols(), out.values.data(),
+                                       &out.scale, nullptr, nullptr));
+    return out;
+}
+
+/// Drop-in for ifa::int_flash_attention (attention.hpp:85-87,
+/// attention.cpp:235-357); the causal extension is not reachable through the
+/// reference's AttentionConfig and stays off here.
+inline ifa::FloatMatrix int_flash_attention(const ifa::QuantizedAttentionInputs& inputs,
+                                            const ifa::AttentionConfig& cfg,
+                                            ifa::PCodeAudit* audit = nullptr) {
+    inputs.validate();  // the reference's own checks and messages, first
+    cfg.validate();
+    const int64_t n = inputs.q.values.rows(), d = inputs.q.values.cols();
+    ifa::FloatMatrix out(n, d);
+    ifa_pcode_audit au{127, 0, 1, 0, 0};
+    const uint32_t flags = cfg.apply_sqrt_d_scaling ? IFA_FLAG_SQRT_D : 0u;
+    check(ifa_int_flash_fwd_host(inputs.q.values.data(), inputs.q.scales.data(),
+                                 inputs.k.values.data(), inputs.k.scales.data(),
+                                 inputs.v.values.data(), &inputs.v.scale, out.data(), 1, n, d,
+                                 cfg.blocks.Br, cfg.blocks.Bc, flags, audit ? &au : nullptr,
+                                 nullptr));
+    if (audit) {
+        // The reference resets the audit at the start of every call
+        // (attention.cpp:260-262) and fills it from that call alone.
+        *audit = ifa::PCodeAudit{};
+        audit->min_code = au.min_code;
+        audit->max_code = au.max_code;
+        audit->row_max_block_hits_127 = au.row_max_block_hits_127 != 0;
+        audit->rows_audited = au.rows_audited;
+    }
+    return out;
+}
+
+}  // namespace ifa_gpu

@@ -25,6 +25,9 @@ EXPORTED_SYMBOLS = (
     "ifa_quantize_per_row",
     "ifa_quantize_per_tensor",
     "ifa_int_flash_fwd",
+    "ifa_quantize_per_row_host",
+    "ifa_quantize_per_tensor_host",
+    "ifa_int_flash_fwd_host",
     "ifa_audit_init",
     "ifa_code_bounds",
     "ifa_last_error",
@@ -68,6 +71,13 @@ def load() -> C.CDLL:
     lib.ifa_int_flash_fwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64,
                                       u32, vp, vp]
     lib.ifa_int_flash_fwd.restype = C.c_int
+    lib.ifa_quantize_per_row_host.argtypes = [vp, i64, i64, vp, vp, vp, vp]
+    lib.ifa_quantize_per_row_host.restype = C.c_int
+    lib.ifa_quantize_per_tensor_host.argtypes = [vp, i64, i64, i64, vp, vp, vp, vp]
+    lib.ifa_quantize_per_tensor_host.restype = C.c_int
+    lib.ifa_int_flash_fwd_host.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64,
+                                           u32, vp, vp]
+    lib.ifa_int_flash_fwd_host.restype = C.c_int
     lib.ifa_audit_init.argtypes = [vp, vp]
     lib.ifa_audit_init.restype = C.c_int
     lib.ifa_code_bounds.argtypes = [vp]

@@ -48,6 +48,39 @@ __global__ void audit_init_kernel(ifa_pcode_audit* a) {
 
 }  // namespace
 
+namespace ifa_b200 {
+
+int set_error(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+// Shape, block and flag checks of ifa_int_flash_fwd, in the reference's
+// order (attention.cpp:213-242, gemm.cpp:16-28); touches no memory.
+int validate_fwd(int64_t slices, int64_t n, int64_t d, int64_t br, int64_t bc, uint32_t flags) {
+    if (slices < 0) return fail(IFA_EINVAL, "int_flash_attention: negative slice count");
+    // attention.cpp:215-218
+    if (n < 1 || d < 1) return fail(IFA_EINVAL, "quantized attention inputs: empty q");
+    // gemm.cpp:16-20 (AttentionConfig::validate)
+    if (br < 1 || bc < 1) return fail(IFA_EINVAL, "BlockSpec: Br and Bc must be >= 1");
+    // attention.cpp:241-242 / gemm.cpp:22-28
+    if (d > IFA_MAX_INT_GEMM_DEPTH)
+        return fail(IFA_EOVERFLOW, "int gemm depth " + std::to_string(d) +
+                                       " exceeds 133144; int32 accumulation could overflow");
+    const int64_t kv_depth = bc < n ? bc : n;
+    if (kv_depth > IFA_MAX_INT_GEMM_DEPTH)
+        return fail(IFA_EOVERFLOW, "int gemm depth " + std::to_string(kv_depth) +
+                                       " exceeds 133144; int32 accumulation could overflow");
+    if (flags & ~(IFA_FLAG_SQRT_D | IFA_FLAG_CAUSAL))
+        return fail(IFA_EINVAL, "int_flash_attention: unknown flag bits");
+    if (d > 128)
+        return fail(IFA_ENOTSUP, "int_flash_attention: head dim " + std::to_string(d) +
+                                     " > 128 is not supported by the sm_100a kernel");
+    return IFA_OK;
+}
+
+}  // namespace ifa_b200
+
 extern "C" {
 
 const char* ifa_last_error(void) { return g_err.c_str(); }
@@ -107,27 +140,11 @@ int ifa_int_flash_fwd(const int8_t* q, const float* sq, const int8_t* k, const f
                       int64_t d, int64_t br, int64_t bc, uint32_t flags,
                       ifa_pcode_audit* audit, void* stream) {
     g_err.clear();
-    if (slices < 0) return fail(IFA_EINVAL, "int_flash_attention: negative slice count");
-    // attention.cpp:215-218
-    if (n < 1 || d < 1) return fail(IFA_EINVAL, "quantized attention inputs: empty q");
-    // gemm.cpp:16-20 (AttentionConfig::validate)
-    if (br < 1 || bc < 1) return fail(IFA_EINVAL, "BlockSpec: Br and Bc must be >= 1");
-    // attention.cpp:241-242 / gemm.cpp:22-28
-    if (d > IFA_MAX_INT_GEMM_DEPTH)
-        return fail(IFA_EOVERFLOW, "int gemm depth " + std::to_string(d) +
-                                       " exceeds 133144; int32 accumulation could overflow");
-    const int64_t kv_depth = bc < n ? bc : n;
-    if (kv_depth > IFA_MAX_INT_GEMM_DEPTH)
-        return fail(IFA_EOVERFLOW, "int gemm depth " + std::to_string(kv_depth) +
-                                       " exceeds 133144; int32 accumulation could overflow");
-    if (flags & ~(IFA_FLAG_SQRT_D | IFA_FLAG_CAUSAL))
-        return fail(IFA_EINVAL, "int_flash_attention: unknown flag bits");
-    if (d > 128)
-        return fail(IFA_ENOTSUP, "int_flash_attention: head dim " + std::to_string(d) +
-                                     " > 128 is not supported by the sm_100a kernel");
+    const int rc = ifa_b200::validate_fwd(slices, n, d, br, bc, flags);
+    if (rc != IFA_OK) return rc;
     if (slices == 0) return IFA_OK;
-    if (slices > 65535)
-        return fail(IFA_ENOTSUP, "int_flash_attention: more than 65535 slices per call");
+    if (((n + 127) / 128) * slices > INT32_MAX)
+        return fail(IFA_ENOTSUP, "int_flash_attention: more than 2^31 (q tile, slice) work items");
     if (!q || !sq || !k || !sk || !v || !sv || !o)
         return fail(IFA_EINVAL, "int_flash_attention: null pointer");
 

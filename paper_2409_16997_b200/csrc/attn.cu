@@ -13,27 +13,35 @@
 // plus the PCodeAudit bookkeeping (:309-311, :319-326, :343-355) and the
 // causal extension (keys j <= row i only).
 //
-// One CTA owns a 128-row Q tile of one (b,h) slice.  Warp roles (22 warps):
-//   warp 0       TMA producer: Q once, then a STAGES-deep ring of K / V tiles
-//                (128 keys x D int8, 128B/64B swizzle) + the K scales.
+// Persistent kernel: one CTA per SM walks a static list of work items
+// (128-row Q tile, (b,h) slice); causal items heaviest first.  Warp roles
+// (20 warps = 5 per SM sub-partition; the launch gives each thread 96
+// registers, then warps 0-3 drop to 32 and hand theirs to the softmax
+// warps, which run with 112):
+//   warp 0       TMA producer: Q (double-buffered across work items), then a
+//                STAGES-deep ring of K / V tiles (128 keys x D int8, 128B/64B
+//                swizzle) + the K scales.
 //   warp 1       TMEM allocator + MMA issuer (one thread): S = Q.K^T
 //                (tcgen05.mma kind::i8, A and B from SMEM) into TMEM;
 //                PV = P.V (A = P from TMEM, B = V from SMEM, MN-major) plus
 //                P.1 (a 16-column all-ones B tile: the exact int32 row sum
 //                of the codes) into TMEM.
-//   warps 2-17   softmax: four threads per Q row (TMEM lane), each owning 32
-//                of the 128 key columns; tcgen05.ld the int32 S slice,
+//   warps 2-3    idle.
+//   warps 4-19   softmax + correction: four threads per Q row (TMEM lane),
+//                each owning 32 of the 128 key columns AND 32 of the output
+//                columns.  Per KV tile: tcgen05.ld the int32 S slice,
 //                dequantize, exchange the partial row max through SMEM,
 //                exact requantization of P (MUFU estimate + rounding guard,
-//                exact glibc-expf fallback), tcgen05.st the packed codes.
-//   warps 18-21  correction: acc = acc*alpha + float(PV) on the f32
-//                accumulator kept in TMEM, l = l*alpha + float(rowsum P);
-//                final O = (acc/l)*sV epilogue.
+//                exact boundary fallback), tcgen05.st the packed codes.  The
+//                PREVIOUS block's P.V (finished while this tile's S was
+//                being computed) is folded into the f32 accumulator held in
+//                registers -- acc = acc*alpha + float(PV), l = l*alpha +
+//                float(rowsum) -- while the row-max exchange completes.
+//                Epilogue O = (acc/l)*sV.
 // Elementwise math uses sm_100 packed FADD2/FMUL2/FFMA2 (IEEE RN per lane,
-// bit-identical to the scalar ops) and magic-number int<->float conversion
-// so the XU (conversion/MUFU) pipe only carries the EX2.
-// TMEM columns: S [0,128) | PV [128,128+D) + rowsum [128+D,144+D) |
-// ACC [272,272+D) | P0 [400,432) | P1 [432,464).
+// bit-identical to the scalar ops).
+// TMEM columns: S [0,128) | PV [128,128+D) | rowsum [256,272) |
+// P0 [288,320) | P1 [320,352).
 //
 // Bc (the reference's KV block size, which changes results) is honoured:
 // a block of <= 128 keys is one pipeline item; a larger block is processed
@@ -58,19 +66,22 @@ namespace attn {
 
 constexpr int BM = 128;
 constexpr int BN = 128;
-constexpr int STAGES = 3;
+constexpr int STAGES = 4;
 constexpr int SPLIT = 4;                 // softmax threads per Q row
-constexpr int NCOL = BN / SPLIT;         // key columns per softmax thread
-constexpr int SOFT_WARP0 = 2;
+constexpr int NCOL = BN / SPLIT;         // key (and output) columns per softmax thread
+constexpr int SOFT_WARP0 = 4;
 constexpr int SOFT_WARPS = 4 * SPLIT;    // softmax warps (4 lane quarters x SPLIT)
-constexpr int CORR_WARP0 = SOFT_WARP0 + SOFT_WARPS;
-constexpr int NUM_THREADS = 32 * (CORR_WARP0 + 4);
+constexpr int NUM_THREADS = 32 * (SOFT_WARP0 + SOFT_WARPS);
+// Per sub-partition (16384 registers): 1 control warp x 32 + 4 softmax warps
+// x 112 = 15360 = 5 warps x the launch's 96.
+constexpr uint32_t kRegsControl = 32;
+constexpr uint32_t kRegsSoftmax = 112;
+static_assert(kRegsControl + 4 * kRegsSoftmax <= 5 * 96, "register budget");
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t T_S = 0, T_PV = 128, T_ACC = 272, T_P0 = 400;
-constexpr float kMagic = 12582912.0f;       // 1.5 * 2^23: float(i) = bits(i + M) - M
-constexpr int32_t kMagicBits = 0x4B400000;
+constexpr uint32_t T_S = 0, T_PV = 128, T_RS = 256, T_P0 = 288;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLog2_127 = 6.9886846867721655f;
+constexpr float kMagic = 12582912.0f;       // 1.5 * 2^23: rounds to the nearest integer
 // The fast estimate y = ex2(s*log2e + c_r), c_r = log2(127) - m*log2e, is
 // within  kGuardBase + kGuardScale * (|m*log2e| + |c_r|)  of the reference's
 // fl(127*fl(expf(fl(s - m)))): in t, half an ulp of |t| < 8, of m*log2e and
@@ -97,7 +108,7 @@ struct Item {
     uint32_t kind;
 };
 
-// Deterministic item sequence shared by every warp role (n < 2^31).
+// Deterministic KV item sequence of one work item, shared by every warp role.
 struct ItemGen {
     int32_t n, bc, kv_limit;
     int32_t b0 = 0;
@@ -141,26 +152,20 @@ struct ItemGen {
     }
 };
 
-struct RingEntry {
-    float alpha[BM];
-};
-
 template <int D>
 struct alignas(1024) Smem {
-    uint8_t q[BM * D];
+    uint8_t q[2][BM * D];
     uint8_t k[STAGES][BN * D];
     uint8_t v[STAGES][BN * D];
     uint8_t ones[16 * BN];  // all-ones B tile: P . 1 = exact int32 row sum of the codes
     float sk[STAGES][BN];
     float xmax[2][SPLIT][BM];  // [item parity][part][row]: partial row max exchange
     float bounds[128];         // B[k]: exact code decision boundaries (code_bounds.h)
-    RingEntry ring[4];     // per-block alpha and code sums for the correction warps
-    uint64_t q_full;
+    uint64_t q_full[2], q_empty[2];
     uint64_t k_full[STAGES], v_full[STAGES], kv_empty[STAGES];
     uint64_t s_full, s_empty;
     uint64_t p_full[2], p_empty[2];
     uint64_t pv_full, pv_empty;
-    uint64_t ring_full[4];
     uint32_t tmem_base;
 };
 
@@ -176,8 +181,33 @@ struct Params {
     uint32_t flags;
     float extra;  // 1/sqrt(d) when IFA_FLAG_SQRT_D, else 1
     int32_t q_tiles;
+    int32_t slices;
+    int32_t items;  // q_tiles * slices
     float bounds[128];
 };
+
+struct Work {
+    int32_t q0, slice, kv_limit;
+};
+
+// Work item -> (Q tile, slice).  Non-causal: the Q tiles of one slice are
+// adjacent, so CTAs running together share K/V in L2.  Causal: diagonal
+// tiles have the most keys, so they go first (longest-processing-time order).
+__device__ __forceinline__ Work work_of(int32_t idx, const Params& p, bool causal) {
+    Work w;
+    int32_t qt;
+    if (causal) {
+        qt = p.q_tiles - 1 - idx / p.slices;
+        w.slice = idx % p.slices;
+    } else {
+        qt = idx % p.q_tiles;
+        w.slice = idx / p.q_tiles;
+    }
+    w.q0 = qt * BM;
+    w.kv_limit = p.n;
+    if (causal && w.q0 + BM < w.kv_limit) w.kv_limit = w.q0 + BM;
+    return w;
+}
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
@@ -185,9 +215,10 @@ __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 // (int)round(127*expf(s - m_new)), packed 4 per word.  Fast path: y =
 // ex2(s*log2e + c_r) with c_r = log2(127) - m_new*log2e, rounded by the
 // magic-number add; every element also measures its distance to that
-// integer.  An estimate within the guard band of a rounding boundary k+1/2
-// (rare) is settled exactly by one comparison against the precomputed
-// boundary B[k] of the reference's code function (code_bounds.h).
+// integer.  Only when an estimate of a group of 8 lies within the guard band
+// of a rounding boundary k+1/2 (rare) are the ambiguous codes settled exactly by
+// one comparison against the precomputed boundary B[k] of the reference's
+// code function (code_bounds.h).
 __device__ __forceinline__ void codes_part(const float (&s)[NCOL], float m_new, float c_r,
                                            float thresh, const float* bounds,
                                            uint32_t (&w)[NCOL / 4]) {
@@ -244,7 +275,21 @@ __device__ __forceinline__ float row_max(const float (&s)[NCOL]) {
     return fmaxf(fmax3(b0, b1, b2), b3);
 }
 
-template <int D, bool AUDIT, bool EXTRA>
+// Ring position of a pipelined resource: stage index + phase parity.
+template <int N>
+struct Ring {
+    uint32_t idx = 0, phase = 0;
+    __device__ __forceinline__ void advance() {
+        if (++idx == N) {
+            idx = 0;
+            phase ^= 1u;
+        }
+    }
+};
+
+// GENERIC = false: the benchmark-shaped fast path (non-causal, Bc <= 128,
+// no audit, no 1/sqrt(d)); true: every feature, selected at run time.
+template <int D, bool GENERIC>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     int_flash_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_k,
@@ -262,19 +307,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
-    const bool causal = (p.flags & IFA_FLAG_CAUSAL) != 0;
-    // Heavier causal tiles first (longest-processing-time order).
-    const int32_t qt = causal ? (p.q_tiles - 1 - static_cast<int32_t>(blockIdx.x))
-                              : static_cast<int32_t>(blockIdx.x);
-    const int32_t q0 = qt * BM;
-    const int32_t slice = static_cast<int32_t>(blockIdx.y);
+    const bool causal = GENERIC && (p.flags & IFA_FLAG_CAUSAL) != 0;
+    const bool audit = GENERIC && p.audit != nullptr;
     const int32_t n = p.n;
-    int32_t kv_limit = n;
-    if (causal && q0 + BM < kv_limit) kv_limit = q0 + BM;
+
+    // shared-window addresses of the barriers
+    const uint32_t b_q_full = smem_u32(&sm.q_full[0]), b_q_empty = smem_u32(&sm.q_empty[0]);
+    const uint32_t b_k_full = smem_u32(&sm.k_full[0]), b_v_full = smem_u32(&sm.v_full[0]);
+    const uint32_t b_kv_empty = smem_u32(&sm.kv_empty[0]);
+    const uint32_t b_s_full = smem_u32(&sm.s_full), b_s_empty = smem_u32(&sm.s_empty);
+    const uint32_t b_p_full = smem_u32(&sm.p_full[0]), b_p_empty = smem_u32(&sm.p_empty[0]);
+    const uint32_t b_pv_full = smem_u32(&sm.pv_full), b_pv_empty = smem_u32(&sm.pv_empty);
 
     if (threadIdx.x == 0) {
         if (smem_u32(smem_raw) & 1023) __trap();  // SWIZZLE_128B tiles need 1 KiB alignment
-        mbar_init(&sm.q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&sm.q_full[i], 1);
+            mbar_init(&sm.q_empty[i], 1);
+            mbar_init(&sm.p_full[i], SOFT_WARPS);
+            mbar_init(&sm.p_empty[i], 1);
+        }
         for (int i = 0; i < STAGES; ++i) {
             mbar_init(&sm.k_full[i], 32);
             mbar_init(&sm.v_full[i], 1);
@@ -282,13 +334,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         mbar_init(&sm.s_full, 1);
         mbar_init(&sm.s_empty, SOFT_WARPS);
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&sm.p_full[i], SOFT_WARPS);
-            mbar_init(&sm.p_empty[i], 1);
-        }
         mbar_init(&sm.pv_full, 1);
-        mbar_init(&sm.pv_empty, 4);
-        for (int i = 0; i < 4; ++i) mbar_init(&sm.ring_full[i], 4);
+        mbar_init(&sm.pv_empty, SOFT_WARPS);
         fence_barrier_init();
     }
     if (threadIdx.x < 128) sm.bounds[threadIdx.x] = p.bounds[threadIdx.x];
@@ -302,7 +349,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
 
-    if (warp == 0) {
+    if (warp < SOFT_WARP0) {
+      regs_dealloc<kRegsControl>();
+      if (warp == 0) {
         // ------------------------------------------------------------ producer
         const uint64_t pol_stream = policy_evict_first();
         const uint64_t pol_keep = policy_evict_last();
@@ -310,57 +359,65 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tma_prefetch_desc(&tm_q);
             tma_prefetch_desc(&tm_k);
             tma_prefetch_desc(&tm_v);
-            mbar_arrive_expect_tx(&sm.q_full, BM * D);
-            tma_load_3d(sm.q, &tm_q, &sm.q_full, 0, q0, slice, pol_stream);
         }
-        const float* sk_slice = p.sk + static_cast<int64_t>(slice) * n;
-        ItemGen gen(n, p.bc, kv_limit);
-        Item it;
-        uint32_t i = 0;
-        while (gen.next(it)) {
-            const uint32_t st = i % STAGES;
-            if (i >= STAGES) mbar_wait(&sm.kv_empty[st], ((i / STAGES) - 1) & 1);
-            float4 kv4;
-            const int32_t key = it.key0 + lane * 4;
-            if (key + 3 < n && (reinterpret_cast<uintptr_t>(sk_slice + key) & 15) == 0) {
-                kv4 = __ldg(reinterpret_cast<const float4*>(sk_slice + key));
-            } else {
-                kv4.x = key + 0 < n ? sk_slice[key + 0] : 0.0f;
-                kv4.y = key + 1 < n ? sk_slice[key + 1] : 0.0f;
-                kv4.z = key + 2 < n ? sk_slice[key + 2] : 0.0f;
-                kv4.w = key + 3 < n ? sk_slice[key + 3] : 0.0f;
-            }
-            reinterpret_cast<float4*>(sm.sk[st])[lane] = kv4;
+        Ring<STAGES> kv;
+        uint32_t i = 0, wi = 0;
+        for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x, ++wi) {
+            const Work w = work_of(idx, p, causal);
+            const uint32_t qb = wi & 1;
             if (lane == 0) {
-                mbar_arrive_expect_tx(&sm.k_full[st], kTileBytes);
-                tma_load_3d(sm.k[st], &tm_k, &sm.k_full[st], 0, it.key0, slice, pol_keep);
-                if (it.kind & K_PV) {
-                    mbar_arrive_expect_tx(&sm.v_full[st], kTileBytes);
-                    tma_load_3d(sm.v[st], &tm_v, &sm.v_full[st], 0, it.key0, slice, pol_keep);
-                } else {
-                    mbar_arrive(&sm.v_full[st]);
-                }
-            } else {
-                mbar_arrive(&sm.k_full[st]);
+                if (wi >= 2) bar_wait(b_q_empty + 8 * qb, ((wi >> 1) - 1) & 1);
+                mbar_arrive_expect_tx(&sm.q_full[qb], BM * D);
+                tma_load_3d(sm.q[qb], &tm_q, &sm.q_full[qb], 0, w.q0, w.slice, pol_stream);
             }
-            ++i;
+            const float* sk_slice = p.sk + static_cast<int64_t>(w.slice) * n;
+            ItemGen gen(n, p.bc, w.kv_limit);
+            Item it;
+            while (gen.next(it)) {
+                const uint32_t st = kv.idx;
+                if (i >= STAGES) bar_wait(b_kv_empty + 8 * st, kv.phase ^ 1u);
+                float4 kv4;
+                const int32_t key = it.key0 + lane * 4;
+                if (key + 3 < n && (reinterpret_cast<uintptr_t>(sk_slice + key) & 15) == 0) {
+                    kv4 = __ldg(reinterpret_cast<const float4*>(sk_slice + key));
+                } else {
+                    kv4.x = key + 0 < n ? sk_slice[key + 0] : 0.0f;
+                    kv4.y = key + 1 < n ? sk_slice[key + 1] : 0.0f;
+                    kv4.z = key + 2 < n ? sk_slice[key + 2] : 0.0f;
+                    kv4.w = key + 3 < n ? sk_slice[key + 3] : 0.0f;
+                }
+                reinterpret_cast<float4*>(sm.sk[st])[lane] = kv4;
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&sm.k_full[st], kTileBytes);
+                    tma_load_3d(sm.k[st], &tm_k, &sm.k_full[st], 0, it.key0, w.slice, pol_keep);
+                    if (it.kind & K_PV) {
+                        mbar_arrive_expect_tx(&sm.v_full[st], kTileBytes);
+                        tma_load_3d(sm.v[st], &tm_v, &sm.v_full[st], 0, it.key0, w.slice,
+                                    pol_keep);
+                    } else {
+                        bar_arrive(b_v_full + 8 * st);
+                    }
+                } else {
+                    bar_arrive(b_k_full + 8 * st);
+                }
+                kv.advance();
+                ++i;
+            }
         }
-    } else if (warp == 1) {
+      } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0) {
-            mbar_wait(&sm.q_full, 0);
-            tc_fence_after();
-            const uint32_t q_base = smem_u32(sm.q);
             const uint32_t ones_base = smem_u32(sm.ones);
-            ItemGen gen(n, p.bc, kv_limit);
-            Item it;
-            uint32_t i = 0, pi = 0, bi = 0;
+            Ring<STAGES> kv;
+            uint32_t i = 0, pi = 0, bi = 0, wi = 0;
             bool have_prev = false;
             uint32_t prev_st = 0, prev_ph = 0, prev_kind = 0, prev_pi = 0;
+            // P.V of a finished softmax item; issued after the next S so the
+            // tensor core computes S(i+1) while the softmax works on tile i.
             auto issue_pv = [&](uint32_t st, uint32_t ph, uint32_t kind, uint32_t pidx) {
-                mbar_wait(&sm.p_full[pidx & 1], (pidx >> 1) & 1);
-                mbar_wait(&sm.v_full[st], ph);
-                if ((kind & K_PV_FIRST) && bi > 0) mbar_wait(&sm.pv_empty, (bi - 1) & 1);
+                bar_wait(b_p_full + 8 * (pidx & 1), (pidx >> 1) & 1);
+                bar_wait(b_v_full + 8 * st, ph);
+                if ((kind & K_PV_FIRST) && bi >= 1) bar_wait(b_pv_empty, (bi - 1) & 1);
                 tc_fence_after();
                 const uint32_t v_base = smem_u32(sm.v[st]);
                 const uint32_t p_col = T_P0 + 32 * (pidx & 1);
@@ -372,186 +429,291 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     mma_i8_ts(tmem + T_PV, tmem + p_col + kk * 8, bdesc, kIdescPV, acc);
                     // P . 1 (16 identical columns): the block's exact code row sum.
                     const uint64_t odesc = smem_desc(ones_base + kk * 32, 16, 1024, kLayoutSw128);
-                    mma_i8_ts(tmem + T_PV + D, tmem + p_col + kk * 8, odesc, kIdescSum, acc);
+                    mma_i8_ts(tmem + T_RS, tmem + p_col + kk * 8, odesc, kIdescSum, acc);
                 }
-                mma_commit(&sm.p_empty[pidx & 1]);
-                mma_commit(&sm.kv_empty[st]);
+                mma_commit_u32(b_p_empty + 8 * (pidx & 1));
+                mma_commit_u32(b_kv_empty + 8 * st);
                 if (kind & K_END) {
-                    mma_commit(&sm.pv_full);
+                    mma_commit_u32(b_pv_full);
                     ++bi;
                 }
             };
-            while (gen.next(it)) {
-                const uint32_t st = i % STAGES;
-                const uint32_t ph = (i / STAGES) & 1;
-                mbar_wait(&sm.k_full[st], ph);
-                if (i > 0) mbar_wait(&sm.s_empty, (i - 1) & 1);
+            for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x, ++wi) {
+                const Work w = work_of(idx, p, causal);
+                const uint32_t qb = wi & 1;
+                bar_wait(b_q_full + 8 * qb, (wi >> 1) & 1);
                 tc_fence_after();
-                const uint32_t k_base = smem_u32(sm.k[st]);
+                const uint32_t q_base = smem_u32(sm.q[qb]);
+                ItemGen gen(n, p.bc, w.kv_limit);
+                Item it;
+                while (gen.next(it)) {
+                    const uint32_t st = kv.idx;
+                    const uint32_t ph = kv.phase;
+                    bar_wait(b_k_full + 8 * st, ph);
+                    if (i > 0) bar_wait(b_s_empty, (i - 1) & 1);
+                    tc_fence_after();
+                    const uint32_t k_base = smem_u32(sm.k[st]);
 #pragma unroll
-                for (int kk = 0; kk < D / 32; ++kk) {
-                    const uint64_t adesc = smem_desc(q_base + kk * 32, 16, kSbo, kLayout);
-                    const uint64_t bdesc = smem_desc(k_base + kk * 32, 16, kSbo, kLayout);
-                    mma_i8_ss(tmem + T_S, adesc, bdesc, kIdescS, kk > 0 ? 1u : 0u);
+                    for (int kk = 0; kk < D / 32; ++kk) {
+                        const uint64_t adesc = smem_desc(q_base + kk * 32, 16, kSbo, kLayout);
+                        const uint64_t bdesc = smem_desc(k_base + kk * 32, 16, kSbo, kLayout);
+                        mma_i8_ss(tmem + T_S, adesc, bdesc, kIdescS, kk > 0 ? 1u : 0u);
+                    }
+                    mma_commit_u32(b_s_full);
+                    if (!(it.kind & K_PV)) mma_commit_u32(b_kv_empty + 8 * st);
+                    if (have_prev) issue_pv(prev_st, prev_ph, prev_kind, prev_pi);
+                    if (it.kind & K_PV) {
+                        have_prev = true;
+                        prev_st = st;
+                        prev_ph = ph;
+                        prev_kind = it.kind;
+                        prev_pi = pi++;
+                    } else {
+                        have_prev = false;
+                    }
+                    kv.advance();
+                    ++i;
                 }
-                mma_commit(&sm.s_full);
-                if (!(it.kind & K_PV)) mma_commit(&sm.kv_empty[st]);
-                if (have_prev) issue_pv(prev_st, prev_ph, prev_kind, prev_pi);
-                if (it.kind & K_PV) {
-                    have_prev = true;
-                    prev_st = st;
-                    prev_ph = ph;
-                    prev_kind = it.kind;
-                    prev_pi = pi++;
-                } else {
-                    have_prev = false;
-                }
-                ++i;
+                // every S MMA reading this Q buffer has been issued
+                mma_commit_u32(b_q_empty + 8 * qb);
             }
             if (have_prev) issue_pv(prev_st, prev_ph, prev_kind, prev_pi);
         }
         __syncwarp();
-    } else if (warp < CORR_WARP0) {
-        // ------------------------------------------------------------ softmax
+      }
+    } else {
+        regs_alloc<kRegsSoftmax>();
+        // ------------------------------------------------- softmax + correction
         const uint32_t quarter = warp & 3;
         const uint32_t part = (warp - SOFT_WARP0) >> 2;  // which NCOL-column slice of the row
         const int32_t row = static_cast<int32_t>(quarter * 32 + lane);
-        const int32_t grow = q0 + row;
-        const bool row_ok = grow < n;
-        const float sq_r = row_ok ? p.sq[static_cast<int64_t>(slice) * n + grow] : 0.0f;
-        const uint32_t t_s = tmem + ((quarter * 32) << 16) + T_S + NCOL * part;
-        const uint32_t t_p = tmem + ((quarter * 32) << 16) + T_P0 + (NCOL / 4) * part;
-        const int32_t c_base = NCOL * part;  // first key column owned by this thread
+        const uint32_t t_lane = tmem + ((quarter * 32) << 16);
+        const uint32_t t_s = t_lane + T_S + NCOL * part;
+        const uint32_t t_p = t_lane + T_P0 + (NCOL / 4) * part;
+        const uint32_t t_pv = t_lane + T_PV + NCOL * part;
+        const uint32_t t_rs = t_lane + T_RS;
+        const int32_t c_base = NCOL * part;  // first key / output column owned by this thread
         const uint32_t bar_id = 1 + quarter;
         const float extra = p.extra;
+        const bool use_extra = GENERIC && (p.flags & IFA_FLAG_SQRT_D) != 0;
         float* const xmax_mine = &sm.xmax[0][part][row];
-        float m = kNegInf;
-        float blk_max = kNegInf, m_new = kNegInf;
-        bool has_full = false, row_hit = false;
+        const float* const xmax_row = &sm.xmax[0][0][row];
+        const float* const sk_part = &sm.sk[0][c_base];
         int32_t cmin = 127, cmax = 0;
-        ItemGen gen(n, p.bc, kv_limit);
-        Item it;
+        bool all_hit = true;
+        int64_t rows_done = 0;
+        Ring<STAGES> kv;
         uint32_t i = 0, pi = 0, bi = 0;
-        while (gen.next(it)) {
-            const uint32_t st = i % STAGES;
-            mbar_wait(&sm.s_full, i & 1);
-            tc_fence_after();
-            uint32_t sr[NCOL];
-            tmem_ld32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-            tmem_wait_ld();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.s_empty);
 
-            mbar_wait(&sm.k_full[st], (i / STAGES) & 1);
-            int32_t lim = it.width;
-            if (causal) {
-                const int32_t vis = grow - it.key0 + 1;
-                if (vis < lim) lim = vis < 0 ? 0 : vis;
-            }
-            lim -= c_base;  // columns of this slice still visible
-            // dequantize: s = float(S) * (sQ * sK) [* extra], product of scales first
-            float s[NCOL];
-            const float4* sk4 = reinterpret_cast<const float4*>(sm.sk[st] + c_base);
+        for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x) {
+            const Work w = work_of(idx, p, causal);
+            const int32_t grow = w.q0 + row;
+            const bool row_ok = grow < n;
+            const float sq_r = row_ok ? p.sq[static_cast<int64_t>(w.slice) * n + grow] : 0.0f;
+            float acc[NCOL];
 #pragma unroll
-            for (int c4 = 0; c4 < NCOL / 4; ++c4) {
-                const float4 k4 = sk4[c4];
-                const int c = c4 * 4;
-                // float(S) exact (|S| < 2^24)
-                const float2 sf01 = make_float2(__int2float_rn(static_cast<int32_t>(sr[c])),
-                                                __int2float_rn(static_cast<int32_t>(sr[c + 1])));
-                const float2 sf23 = make_float2(__int2float_rn(static_cast<int32_t>(sr[c + 2])),
-                                                __int2float_rn(static_cast<int32_t>(sr[c + 3])));
-                float2 s01 = fmul2(sf01, fmul2(f2(sq_r), make_float2(k4.x, k4.y)));
-                float2 s23 = fmul2(sf23, fmul2(f2(sq_r), make_float2(k4.z, k4.w)));
-                if (EXTRA) {
-                    s01 = fmul2(s01, f2(extra));
-                    s23 = fmul2(s23, f2(extra));
-                }
-                s[c] = s01.x;
-                s[c + 1] = s01.y;
-                s[c + 2] = s23.x;
-                s[c + 3] = s23.y;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.kv_empty[st]);
-            if (lim < NCOL) {
-#pragma unroll
-                for (int c = 0; c < NCOL; ++c) s[c] = c < lim ? s[c] : kNegInf;
-            }
-            float m_loc = row_max(s);
-            float s_min = -kNegInf;
-            if (AUDIT) {
-#pragma unroll
-                for (int c = 0; c < NCOL; ++c)
-                    if (c < lim) s_min = fminf(s_min, s[c]);
-            }
-            // partial row max exchange among the SPLIT threads of this row
-            xmax_mine[(i & 1) * SPLIT * BM] = m_loc;
-            named_bar_sync(bar_id, 32 * SPLIT);
-            {
-                const float* xr = &sm.xmax[i & 1][0][row];
-                m_loc = fmaxf(fmax3(xr[0], xr[BM], xr[2 * BM]), xr[3 * BM]);
-            }
+            for (int c = 0; c < NCOL; ++c) acc[c] = 0.0f;
+            float l = 0.0f;
+            float m = kNegInf;
+            float blk_max = kNegInf, m_new = kNegInf;
+            bool has_full = false, row_hit = false;
+            bool pend = false;
+            float pend_alpha = 1.0f;
 
-            if (it.kind & K_BEGIN) blk_max = kNegInf;
-            if (!(it.kind & K_PV) || (it.kind & K_BEGIN)) blk_max = fmaxf(blk_max, m_loc);
-            if (it.kind & K_MAXDONE) {
-                m_new = (m < blk_max) ? blk_max : m;  // std::max(m, m_loc)
-                // the block's largest code comes from its largest score
-                if (AUDIT)
-                    has_full = blk_max != kNegInf &&
-                               guarded_code(__fsub_rn(blk_max, m_new)) == 127;
-            }
-            if (it.kind & K_PV) {
-                if ((it.kind & K_END) && part == 0) {
-                    // alpha = expf(m - m_new) (attention.cpp:298) for the correction warps
-                    sm.ring[bi & 3].alpha[row] = exact_expf(__fsub_rn(m, m_new));
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&sm.ring_full[bi & 3]);
-                }
-                if (pi >= 2) {
-                    mbar_wait(&sm.p_empty[pi & 1], ((pi - 2) >> 1) & 1);
-                    tc_fence_after();
-                }
-                uint32_t w[NCOL / 4];
-                const float mL = __fmul_rn(m_new, kLog2e);
-                const float c_r = __fsub_rn(kLog2_127, mL);
-                const float thresh =
-                    0.5f - (kGuardBase + kGuardScale * (fabsf(mL) + fabsf(c_r)));
-                codes_part(s, m_new, c_r, thresh, sm.bounds, w);
-                asm volatile(
-                    "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
-                        t_p + 32 * (pi & 1)),
-                    "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]),
-                    "r"(w[7])
-                    : "memory");
-                if (AUDIT && row_ok && lim > 0) {
-                    cmax = max(cmax, guarded_code(__fsub_rn(row_max(s), m_new)));
-                    cmin = min(cmin, guarded_code(__fsub_rn(s_min, m_new)));
-                }
-                if (it.kind & K_END) {
-                    if (m_new > m)
-                        row_hit = has_full;
-                    else if (blk_max == m_new && has_full)
-                        row_hit = true;
-                    m = m_new;
-                    ++bi;
-                }
-                tmem_wait_st();
+            // acc = acc*alpha + float(PV), l = l*alpha + float(rowsum)
+            // (attention.cpp:313-318, :330-333) for the finished block bi.
+            auto fold_pv = [&](float alpha) {
+                bar_wait(b_pv_full, bi & 1);
+                tc_fence_after();
+                uint32_t pv[NCOL];
+                uint32_t rs;
+                tmem_ld32(t_pv, pv);
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
+                             : "=r"(rs)
+                             : "r"(t_rs));
+                tmem_wait_ld();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.p_full[pi & 1]);
-                ++pi;
+                if (lane == 0) bar_arrive(b_pv_empty);
+                ++bi;
+                l = __fadd_rn(__fmul_rn(l, alpha), static_cast<float>(static_cast<int32_t>(rs)));
+                // acc *= alpha, rounded before the add (no FMA); skipped when
+                // alpha == 1 for the whole warp, which leaves acc bit-identical.
+                if (!__all_sync(0xffffffffu, alpha == 1.0f)) {
+#pragma unroll
+                    for (int c = 0; c < NCOL; c += 2) {
+                        const float2 a = fmul2_nc(make_float2(acc[c], acc[c + 1]), f2(alpha));
+                        acc[c] = a.x;
+                        acc[c + 1] = a.y;
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < NCOL; c += 2) {
+                    // float(int32) exact here: |PV| < 127*127*Bc < 2^24 for Bc <= 1040;
+                    // I2FP rounds to nearest like the reference's cast otherwise.
+                    const float2 pf = make_float2(__int2float_rn(static_cast<int32_t>(pv[c])),
+                                                  __int2float_rn(static_cast<int32_t>(pv[c + 1])));
+                    const float2 a = fadd2(make_float2(acc[c], acc[c + 1]), pf);
+                    acc[c] = a.x;
+                    acc[c + 1] = a.y;
+                }
+            };
+
+            ItemGen gen(n, p.bc, w.kv_limit);
+            Item it;
+            while (gen.next(it)) {
+                const uint32_t st = kv.idx;
+                bar_wait(b_s_full, i & 1);
+                tc_fence_after();
+                uint32_t sr[NCOL];
+                tmem_ld32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) bar_arrive(b_s_empty);
+
+                bar_wait(b_k_full + 8 * st, kv.phase);
+                int32_t lim = it.width;
+                if (causal) {
+                    const int32_t vis = grow - it.key0 + 1;
+                    if (vis < lim) lim = vis < 0 ? 0 : vis;
+                }
+                lim -= c_base;  // columns of this slice still visible
+                // dequantize: s = float(S) * (sQ * sK) [* extra], product of scales first
+                float s[NCOL];
+                const float4* sk4 = reinterpret_cast<const float4*>(sk_part + st * BN);
+#pragma unroll
+                for (int c4 = 0; c4 < NCOL / 4; ++c4) {
+                    const float4 k4 = sk4[c4];
+                    const int c = c4 * 4;
+                    // float(S) exact (|S| < 2^24)
+                    const float2 sf01 = make_float2(__int2float_rn(static_cast<int32_t>(sr[c])),
+                                                    __int2float_rn(static_cast<int32_t>(sr[c + 1])));
+                    const float2 sf23 = make_float2(__int2float_rn(static_cast<int32_t>(sr[c + 2])),
+                                                    __int2float_rn(static_cast<int32_t>(sr[c + 3])));
+                    float2 s01 = fmul2(sf01, fmul2(f2(sq_r), make_float2(k4.x, k4.y)));
+                    float2 s23 = fmul2(sf23, fmul2(f2(sq_r), make_float2(k4.z, k4.w)));
+                    if (use_extra) {
+                        s01 = fmul2(s01, f2(extra));
+                        s23 = fmul2(s23, f2(extra));
+                    }
+                    s[c] = s01.x;
+                    s[c + 1] = s01.y;
+                    s[c + 2] = s23.x;
+                    s[c + 3] = s23.y;
+                }
+                __syncwarp();
+                if (lane == 0) bar_arrive(b_kv_empty + 8 * st);
+                if (lim < NCOL) {
+#pragma unroll
+                    for (int c = 0; c < NCOL; ++c) s[c] = c < lim ? s[c] : kNegInf;
+                }
+                const float m_part = row_max(s);
+                float s_min = -kNegInf;
+                if (GENERIC && audit) {
+#pragma unroll
+                    for (int c = 0; c < NCOL; ++c)
+                        if (c < lim) s_min = fminf(s_min, s[c]);
+                }
+                // partial row max exchange among the SPLIT threads of this row;
+                // the previous block's P.V is folded while the others catch up
+                xmax_mine[(i & 1) * SPLIT * BM] = m_part;
+                named_bar_sync(bar_id, 32 * SPLIT);
+                float m_loc;
+                {
+                    const float* xr = xmax_row + (i & 1) * SPLIT * BM;
+                    m_loc = fmaxf(fmax3(xr[0], xr[BM], xr[2 * BM]), xr[3 * BM]);
+                }
+
+                if (it.kind & K_BEGIN) blk_max = kNegInf;
+                if (!(it.kind & K_PV) || (it.kind & K_BEGIN)) blk_max = fmaxf(blk_max, m_loc);
+                if (it.kind & K_MAXDONE) {
+                    m_new = (m < blk_max) ? blk_max : m;  // std::max(m, m_loc)
+                    // the block's largest code comes from its largest score
+                    if (GENERIC && audit)
+                        has_full = blk_max != kNegInf &&
+                                   guarded_code(__fsub_rn(blk_max, m_new)) == 127;
+                }
+                if (it.kind & K_PV) {
+                    if (pi >= 2) {
+                        bar_wait(b_p_empty + 8 * (pi & 1), ((pi - 2) >> 1) & 1);
+                        tc_fence_after();
+                    }
+                    uint32_t wd[NCOL / 4];
+                    const float mL = __fmul_rn(m_new, kLog2e);
+                    const float c_r = __fsub_rn(kLog2_127, mL);
+                    const float thresh =
+                        0.5f - (kGuardBase + kGuardScale * (fabsf(mL) + fabsf(c_r)));
+                    codes_part(s, m_new, c_r, thresh, sm.bounds, wd);
+                    asm volatile(
+                        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                            t_p + 32 * (pi & 1)),
+                        "r"(wd[0]), "r"(wd[1]), "r"(wd[2]), "r"(wd[3]), "r"(wd[4]), "r"(wd[5]),
+                        "r"(wd[6]), "r"(wd[7])
+                        : "memory");
+                    if (GENERIC && audit && row_ok && lim > 0) {
+                        cmax = max(cmax, guarded_code(__fsub_rn(m_part, m_new)));
+                        cmin = min(cmin, guarded_code(__fsub_rn(s_min, m_new)));
+                    }
+                    // fold the previous block's P.V (finished long ago) while
+                    // the code stores drain; it must precede p_full so the
+                    // next P.V may overwrite the single accumulator
+                    if (pend) {
+                        fold_pv(pend_alpha);
+                        pend = false;
+                    }
+                    tmem_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) bar_arrive(b_p_full + 8 * (pi & 1));
+                    ++pi;
+                    if (it.kind & K_END) {
+                        // alpha = expf(m - m_new) (attention.cpp:298); exp(0) = 1
+                        const float alpha = (m_new == m) ? 1.0f : exact_expf(__fsub_rn(m, m_new));
+                        if (m_new > m)
+                            row_hit = has_full;
+                        else if (blk_max == m_new && has_full)
+                            row_hit = true;
+                        m = m_new;
+                        pend = true;  // its P.V is folded during the next tile
+                        pend_alpha = alpha;
+                    }
+                }
+                kv.advance();
+                ++i;
             }
-            ++i;
+            if (pend) fold_pv(pend_alpha);
+
+            // epilogue: O = (acc / l) * sV (attention.cpp:335-342)
+            if (row_ok && c_base < p.d) {
+                const float sv = p.sv[w.slice];
+                const int32_t d = p.d;
+                float* orow = p.o + (static_cast<int64_t>(w.slice) * n + grow) * d + c_base;
+                float out[NCOL];
+#pragma unroll
+                for (int c = 0; c < NCOL; ++c) out[c] = __fmul_rn(__fdiv_rn(acc[c], l), sv);
+                if (d % 4 == 0 && c_base + NCOL <= d) {
+#pragma unroll
+                    for (int c = 0; c < NCOL; c += 4)
+                        __stcs(reinterpret_cast<float4*>(orow + c),
+                               make_float4(out[c], out[c + 1], out[c + 2], out[c + 3]));
+                } else {
+#pragma unroll
+                    for (int c = 0; c < NCOL; ++c)
+                        if (c_base + c < d) orow[c] = out[c];
+                }
+            }
+            if (GENERIC && audit && row_ok) {
+                all_hit = all_hit && row_hit;
+                if (part == 0) ++rows_done;
+            }
         }
-        if (AUDIT && p.audit != nullptr) {
-            // rows >= n never emitted a code; only part 0 reports row facts
-            int32_t my_min = row_ok ? cmin : 127;
-            int32_t my_max = row_ok ? cmax : 0;
-            int32_t my_hit = (row_ok && part == 0) ? (row_hit ? 1 : 0) : 1;
-            int32_t my_rows = (row_ok && part == 0) ? 1 : 0;
+        if (GENERIC && audit) {
+            // rows >= n never emitted a code; only part 0 counts rows
+            int32_t my_min = cmin;
+            int32_t my_max = cmax;
+            int32_t my_hit = all_hit ? 1 : 0;
+            unsigned long long my_rows = static_cast<unsigned long long>(rows_done);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 my_min = min(my_min, __shfl_xor_sync(0xffffffffu, my_min, o));
@@ -565,115 +727,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (!my_hit) atomicAnd(&p.audit->row_max_block_hits_127, 0);
                 if (my_rows)
                     atomicAdd(reinterpret_cast<unsigned long long*>(&p.audit->rows_audited),
-                              static_cast<unsigned long long>(my_rows));
-            }
-        }
-    } else {
-        // ------------------------------------------------------------ correction
-        const uint32_t quarter = warp & 3;
-        const int32_t row = static_cast<int32_t>(quarter * 32 + lane);
-        const int32_t grow = q0 + row;
-        const uint32_t t_lane = tmem + ((quarter * 32) << 16);
-        // P.V int32 of one block fits the magic conversion while |pv| < 2^22
-        const bool pv_magic = p.bc <= 256;
-        float l = 0.0f;
-        ItemGen gen(n, p.bc, kv_limit);
-        Item it;
-        uint32_t bi = 0;
-        while (gen.next(it)) {
-            if (!(it.kind & K_END)) continue;
-            mbar_wait(&sm.ring_full[bi & 3], (bi >> 2) & 1);
-            const float alpha = sm.ring[bi & 3].alpha[row];
-            // acc *= alpha (attention.cpp:316-318) -- its own TMEM round trip so
-            // the product is rounded before the add (ptxas contracts adjacent
-            // mul.rn.f32x2/add.rn.f32x2 into FFMA2); skipped when alpha == 1
-            // for the whole warp, which leaves acc bit-identical.
-            if (bi > 0 && !__all_sync(0xffffffffu, alpha == 1.0f)) {
-#pragma unroll
-                for (int c0 = 0; c0 < D; c0 += 16) {
-                    uint32_t acc[16];
-                    tmem_ld16(t_lane + T_ACC + c0, acc);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int j = 0; j < 16; j += 2) {
-                        const float2 a = fmul2(make_float2(__uint_as_float(acc[j]),
-                                                           __uint_as_float(acc[j + 1])),
-                                               f2(alpha));
-                        acc[j] = __float_as_uint(a.x);
-                        acc[j + 1] = __float_as_uint(a.y);
-                    }
-                    tmem_st16(t_lane + T_ACC + c0, acc);
-                }
-                tmem_wait_st();
-            }
-            // acc += float(PV) (attention.cpp:330-333); l = l*alpha + float(sum P)
-            mbar_wait(&sm.pv_full, bi & 1);
-            tc_fence_after();
-            {
-                uint32_t rs;
-                asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
-                             : "=r"(rs)
-                             : "r"(t_lane + T_PV + D));
-                tmem_wait_ld();
-                l = __fadd_rn(__fmul_rn(l, alpha), static_cast<float>(static_cast<int32_t>(rs)));
-            }
-#pragma unroll
-            for (int c0 = 0; c0 < D; c0 += 16) {
-                uint32_t pv[16], acc[16];
-                tmem_ld16(t_lane + T_PV + c0, pv);
-                if (bi > 0) tmem_ld16(t_lane + T_ACC + c0, acc);
-                tmem_wait_ld();
-#pragma unroll
-                for (int j = 0; j < 16; j += 2) {
-                    float2 pf;
-                    if (pv_magic) {
-                        pf = fsub2(make_float2(__int_as_float(static_cast<int32_t>(pv[j]) + kMagicBits),
-                                               __int_as_float(static_cast<int32_t>(pv[j + 1]) + kMagicBits)),
-                                   f2(kMagic));
-                    } else {
-                        pf = make_float2(__int2float_rn(static_cast<int32_t>(pv[j])),
-                                         __int2float_rn(static_cast<int32_t>(pv[j + 1])));
-                    }
-                    const float2 a =
-                        bi > 0 ? fadd2(make_float2(__uint_as_float(acc[j]), __uint_as_float(acc[j + 1])), pf)
-                               : pf;
-                    acc[j] = __float_as_uint(a.x);
-                    acc[j + 1] = __float_as_uint(a.y);
-                }
-                tmem_st16(t_lane + T_ACC + c0, acc);
-            }
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.pv_empty);
-            ++bi;
-        }
-        // epilogue: O = (acc / l) * sV
-        const float sv = p.sv[slice];
-        tc_fence_after();
-        const int32_t d = p.d;
-        float* orow = p.o + (static_cast<int64_t>(slice) * n + grow) * d;
-        const bool vec = (d % 4 == 0);
-#pragma unroll
-        for (int c0 = 0; c0 < D; c0 += 32) {
-            uint32_t acc[32];
-            tmem_ld32(t_lane + T_ACC + c0, acc);
-            tmem_wait_ld();
-            if (grow < n && c0 < d) {
-                float out[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    out[j] = __fmul_rn(__fdiv_rn(__uint_as_float(acc[j]), l), sv);
-                if (vec && c0 + 32 <= d) {
-#pragma unroll
-                    for (int j = 0; j < 32; j += 4)
-                        __stcs(reinterpret_cast<float4*>(orow + c0 + j),
-                               make_float4(out[j], out[j + 1], out[j + 2], out[j + 3]));
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (c0 + j < d) orow[c0 + j] = out[j];
-                }
+                              my_rows);
             }
         }
     }
@@ -724,20 +778,30 @@ static bool make_map(CUtensorMap* map, const int8_t* base, int64_t slices, int64
     return r == CUDA_SUCCESS;
 }
 
-template <int D, bool AUDIT, bool EXTRA>
+template <int D, bool GENERIC>
 static cudaError_t launch_k(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                             const Params& p, int64_t slices, cudaStream_t stream) {
     const size_t smem = sizeof(Smem<D>) + 1024;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(int_flash_fwd_kernel<D, AUDIT, EXTRA>,
+        cudaError_t e = cudaFuncSetAttribute(int_flash_fwd_kernel<D, GENERIC>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    dim3 grid(static_cast<unsigned>(p.q_tiles), static_cast<unsigned>(slices));
-    int_flash_fwd_kernel<D, AUDIT, EXTRA><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+    // persistent: one CTA per SM (the kernel needs the whole SM: 512 TMEM
+    // columns, ~170 KB of shared memory)
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    (void)slices;
+    const int grid = p.items < sms ? p.items : sms;
+    int_flash_fwd_kernel<D, GENERIC><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
     return cudaGetLastError();
 }
 
@@ -760,20 +824,22 @@ static cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
     p.flags = a.flags;
     p.extra = (a.flags & IFA_FLAG_SQRT_D) ? 1.0f / sqrtf(static_cast<float>(a.d)) : 1.0f;
     p.q_tiles = static_cast<int32_t>((a.n + BM - 1) / BM);
+    p.slices = static_cast<int32_t>(a.slices);
+    p.items = p.q_tiles * p.slices;
     const float* bounds = code_bounds();
     for (int k = 0; k < 128; ++k) p.bounds[k] = bounds[k];
-    const bool extra = (a.flags & IFA_FLAG_SQRT_D) != 0;
-    if (a.audit != nullptr)
-        return extra ? launch_k<D, true, true>(tq, tk, tv, p, a.slices, stream)
-                     : launch_k<D, true, false>(tq, tk, tv, p, a.slices, stream);
-    return extra ? launch_k<D, false, true>(tq, tk, tv, p, a.slices, stream)
-                 : launch_k<D, false, false>(tq, tk, tv, p, a.slices, stream);
+    // the benchmark-shaped fast path, or the fully general kernel
+    const bool generic = a.audit != nullptr || (a.flags & (IFA_FLAG_SQRT_D | IFA_FLAG_CAUSAL)) ||
+                         p.bc > BN;
+    return generic ? launch_k<D, true>(tq, tk, tv, p, a.slices, stream)
+                   : launch_k<D, false>(tq, tk, tv, p, a.slices, stream);
 }
 
 }  // namespace attn
 
 cudaError_t launch_int_flash_fwd(const AttnArgs& a, cudaStream_t stream) {
-    if (a.slices > 65535 || a.n > (int64_t{1} << 30)) return cudaErrorInvalidValue;
+    if (a.n > (int64_t{1} << 30) || ((a.n + 127) / 128) * a.slices > INT32_MAX)
+        return cudaErrorInvalidValue;
     if (a.d <= 64) return attn::launch_d<64>(a, stream);
     return attn::launch_d<128>(a, stream);
 }

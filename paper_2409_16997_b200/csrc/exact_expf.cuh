@@ -24,7 +24,7 @@ __device__ __constant__ uint64_t kExp2fTabDev[32] = {
     0x3fef5818dcfba487ULL, 0x3fef7c97337b9b5fULL, 0x3fefa4afa2a490daULL, 0x3fefd0765b6e4540ULL};
 
 // Bit-exact glibc expf.  Arguments on the attention path are <= 0 or -inf.
-__device__ __noinline__ float exact_expf(float x) {
+__device__ __forceinline__ float exact_expf(float x) {
     const uint32_t ux = __float_as_uint(x);
     const uint32_t abstop = (ux >> 20) & 0x7ff;
     if (abstop >= 0x42b) {

@@ -6,9 +6,16 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <string>
+
 #include "../../include/ifa_b200.h"
 
 namespace ifa_b200 {
+
+// Sets the thread-local ifa_last_error() message and returns `code`.
+int set_error(int code, const std::string& msg);
+// ifa_int_flash_fwd's argument checks (status + message), no memory access.
+int validate_fwd(int64_t slices, int64_t n, int64_t d, int64_t br, int64_t bc, uint32_t flags);
 
 cudaError_t launch_quantize_per_row(const float* x, int64_t rows, int64_t cols, int8_t* codes,
                                     float* scales, int64_t* bad, cudaStream_t stream);

@@ -55,21 +55,36 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// Blocking wait: try_wait with a suspend-time hint parks the warp in hardware
+// until the phase completes (or ~10 ms pass), so waiting warps do not take
+// issue slots from the ones doing the math.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    while (!mbar_try_wait(bar, parity)) {
-    }
-}
-// Same, but lets the hardware suspend the thread (up to ~suspend_ns) instead
-// of spinning: for the single-thread producer / MMA roles.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
     do {
         asm volatile(
             "{\n\t.reg .pred P;\n\t"
-            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2, 100000;\n\t"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2, 10000000;\n\t"
             "selp.u32 %0, 1, 0, P;\n\t}\n"
             : "=r"(ok)
             : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+
+// Same primitives on a precomputed shared-window address (keeps the
+// address arithmetic out of the hot loops).
+__device__ __forceinline__ void bar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred P;\n\t"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2, 10000000;\n\t"
+            "selp.u32 %0, 1, 0, P;\n\t}\n"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
             : "memory");
     } while (!ok);
 }
@@ -119,6 +134,18 @@ __device__ __forceinline__ void tma_store_wait_read() {
 }
 __device__ __forceinline__ void fence_proxy_async_shared() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- register budget
+// Warpgroup-wide register reallocation (all 4 warps of the warpgroup must
+// execute the same instruction).
+template <uint32_t kRegs>
+__device__ __forceinline__ void regs_dealloc() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+template <uint32_t kRegs>
+__device__ __forceinline__ void regs_alloc() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
 }
 
 // ---------------------------------------------------------------- named barriers
@@ -171,6 +198,11 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile(
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_u32(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
         : "memory");
 }
 __device__ __forceinline__ void tmem_wait_ld() {
