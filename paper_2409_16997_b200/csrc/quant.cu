@@ -8,10 +8,23 @@
 // (nvcc -prec-div=true, no fast-math); max is order independent, so the
 // parallel reductions below are bit-identical to the serial loop.
 //
-// Per-row (Q, K): one warp per row, 128-bit loads, codes packed four per
-// 32-bit store.  Per-tensor (V, one scale per (b,h) slice): slice absmax by
-// an unsigned atomicMax on the float bits (all values are >= 0), then a
-// quantize pass.
+// Division: the IEEE quotient is only needed where it decides a rounding.
+// Each row (or slice) computes r = RN(1/scale) once; per element q0 =
+// RN(x*r) is within 2^-23*|x/scale| <= 1.6e-5 of the exact quotient and so
+// within 2.4e-5 of the reference's RN(x/scale).  Whenever q0 is farther than
+// kDivGuard from a half-integer, round(q0) IS the reference's code; the
+// (rare) others are recomputed with the IEEE division itself.  A scale whose
+// reciprocal overflows takes the IEEE path for the whole row.
+//
+// Per-row (Q, K), cols in {32, 64, 128, 256}: eight lanes per row, four rows
+// per warp step, every lane holding its whole share of the row (128-bit
+// streaming loads), codes packed four per 32-bit store.  Other shapes: one
+// warp per row.  Per-tensor (V, one scale per (b,h) slice): a cluster of 8
+// CTAs per slice, partial maxima exchanged through distributed shared memory,
+// then the quantize pass re-reads the slice from L2.  Non-finite input is
+// detected with a NaN-propagating max, then located exactly (rare path).
+#include <algorithm>
+#include <cooperative_groups.h>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -36,6 +49,34 @@ __device__ __forceinline__ uint32_t pack4(float a, float b, float c, float d, fl
 __device__ __forceinline__ void note_nonfinite(float v, int64_t idx, int64_t* bad) {
     if (!isfinite(v) && bad != nullptr)
         atomicMin(reinterpret_cast<unsigned long long*>(bad), static_cast<unsigned long long>(idx));
+}
+
+constexpr float kDivGuard = 0.5f - 4.0e-5f;
+constexpr float kMagicF = 12582912.0f;  // 1.5 * 2^23
+
+// |a| max that propagates NaN (max.NaN.f32), so one check per row finds it.
+__device__ __forceinline__ float absmax_nan(float m, float a, float b) {
+    float d;
+    asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(m), "f"(fabsf(a)), "f"(fabsf(b)));
+    return d;
+}
+
+// Codes of 4 values: fast estimate + exact fallback.  Returns the packed word.
+__device__ __forceinline__ uint32_t codes4(float4 v, float scale, float rcp, bool exact_row) {
+    const float q[4] = {__fmul_rn(v.x, rcp), __fmul_rn(v.y, rcp), __fmul_rn(v.z, rcp),
+                        __fmul_rn(v.w, rcp)};
+    uint32_t b[4];
+    float g = 0.0f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float t = __fadd_rn(q[e], kMagicF);
+        g = fmaxf(g, fabsf(__fsub_rn(q[e], __fsub_rn(t, kMagicF))));
+        b[e] = __float_as_uint(t);
+    }
+    uint32_t w = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040),
+                             0x5410);
+    if (exact_row || !(g <= kDivGuard)) w = pack4(v.x, v.y, v.z, v.w, scale);
+    return w;
 }
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -175,6 +216,124 @@ __global__ void __launch_bounds__(256) slice_quantize_kernel(const float* __rest
     }
 }
 
+// Eight lanes per row, four rows per warp step: cols == 32 * NV.
+template <int NV>
+__global__ void __launch_bounds__(256) quantize_rows8_kernel(const float* __restrict__ x,
+                                                             int64_t rows,
+                                                             int8_t* __restrict__ codes,
+                                                             float* __restrict__ scales,
+                                                             int64_t* bad) {
+    constexpr int64_t kCols = 32 * NV;
+    const int lane = threadIdx.x & 31, l8 = lane & 7;
+    const int64_t warps_total = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t r0 = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4;
+         r0 < rows; r0 += warps_total * 4) {
+        const int64_t row = r0 + (lane >> 3);
+        const bool ok = row < rows;
+        const float4* src = reinterpret_cast<const float4*>(x + row * kCols);
+        float4 v[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+            v[j] = ok ? __ldcs(src + l8 + 8 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float m = 0.0f;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) m = absmax_nan(absmax_nan(m, v[j].x, v[j].y), v[j].z, v[j].w);
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+            const float other = __shfl_xor_sync(0xffffffffu, m, o);
+            asm("max.NaN.f32 %0, %0, %1;" : "+f"(m) : "f"(other));
+        }
+        if (!(m <= 3.402823466e38f)) {  // NaN or Inf in the row: locate it exactly
+            if (ok) {
+#pragma unroll
+                for (int j = 0; j < NV; ++j) {
+                    const int64_t base = row * kCols + 4 * (l8 + 8 * j);
+                    note_nonfinite(v[j].x, base + 0, bad);
+                    note_nonfinite(v[j].y, base + 1, bad);
+                    note_nonfinite(v[j].z, base + 2, bad);
+                    note_nonfinite(v[j].w, base + 3, bad);
+                }
+            }
+        }
+        const float scale = __fdiv_rn(m, 127.0f);
+        if (ok && l8 == 0) scales[row] = scale;
+        const float rcp = __frcp_rn(scale);
+        const bool exact_row = !(rcp <= 3.402823466e38f);  // scale 0 / denormal / non-finite
+        uint32_t* dst = reinterpret_cast<uint32_t*>(codes + row * kCols);
+        if (ok) {
+#pragma unroll
+            for (int j = 0; j < NV; ++j) dst[l8 + 8 * j] = codes4(v[j], scale, rcp, exact_row);
+        }
+    }
+}
+
+// V: one cluster of kSliceCluster CTAs per slice.  Pass 1: partial abs max
+// of this CTA's chunk; the cluster combines the partials through DSMEM.
+// Pass 2: quantize the chunk (re-read, now L2-resident).
+constexpr int kSliceCluster = 8;
+__global__ void __cluster_dims__(kSliceCluster, 1, 1) __launch_bounds__(512)
+    slice_quantize_fused_kernel(const float* __restrict__ x, int64_t slice_elems,
+                                int8_t* __restrict__ codes, float* __restrict__ slice_scales,
+                                int64_t* bad) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    __shared__ float red[16];
+    __shared__ float part;
+    const int64_t slice = blockIdx.x / kSliceCluster;
+    const int rank = static_cast<int>(cluster.block_rank());
+    const int64_t n4 = slice_elems >> 2;
+    const int64_t per = (n4 + kSliceCluster - 1) / kSliceCluster;
+    const int64_t lo = rank * per;
+    const int64_t hi = lo + per < n4 ? lo + per : n4;
+    const float4* src = reinterpret_cast<const float4*>(x + slice * slice_elems);
+    float m = 0.0f;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const float4 v = src[i];
+        m = absmax_nan(absmax_nan(m, v.x, v.y), v.z, v.w);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float other = __shfl_xor_sync(0xffffffffu, m, o);
+        asm("max.NaN.f32 %0, %0, %1;" : "+f"(m) : "f"(other));
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float other = __shfl_xor_sync(0xffffffffu, v, o);
+            asm("max.NaN.f32 %0, %0, %1;" : "+f"(v) : "f"(other));
+        }
+        if (threadIdx.x == 0) part = v;
+    }
+    cluster.sync();
+    float sm = 0.0f;
+#pragma unroll
+    for (int r = 0; r < kSliceCluster; ++r) {
+        const float other = *cluster.map_shared_rank(&part, r);
+        asm("max.NaN.f32 %0, %0, %1;" : "+f"(sm) : "f"(other));
+    }
+    const float scale = __fdiv_rn(sm, 127.0f);
+    if (rank == 0 && threadIdx.x == 0) slice_scales[slice] = scale;
+    if (!(sm <= 3.402823466e38f) && !(part <= 3.402823466e38f)) {  // locate it exactly
+        for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+            const float4 v = src[i];
+            const int64_t base = slice * slice_elems + 4 * i;
+            note_nonfinite(v.x, base + 0, bad);
+            note_nonfinite(v.y, base + 1, bad);
+            note_nonfinite(v.z, base + 2, bad);
+            note_nonfinite(v.w, base + 3, bad);
+        }
+    }
+    const float rcp = __frcp_rn(scale);
+    const bool exact_row = !(rcp <= 3.402823466e38f);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(codes + slice * slice_elems);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
+        dst[i] = codes4(__ldcs(src + i), scale, rcp, exact_row);
+    cluster.sync();  // keep this CTA's `part` alive until every peer has read it
+}
+
 // ------------------------------------------------------------------ launchers
 static int sm_count() {
     static int n = 0;
@@ -197,7 +356,14 @@ cudaError_t launch_quantize_per_row(const float* x, int64_t rows, int64_t cols, 
     if (blocks > cap) blocks = cap;
     const bool vec = (cols % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(codes) % 4 == 0);
-    if (vec && cols <= 128)
+    const int64_t blocks8 = std::min<int64_t>((rows + 31) / 32, static_cast<int64_t>(sm_count()) * 8);
+    if (vec && (reinterpret_cast<uintptr_t>(codes) % 16 == 0) && cols == 128)
+        quantize_rows8_kernel<4><<<blocks8, threads, 0, stream>>>(x, rows, codes, scales, bad);
+    else if (vec && (reinterpret_cast<uintptr_t>(codes) % 16 == 0) && cols == 64)
+        quantize_rows8_kernel<2><<<blocks8, threads, 0, stream>>>(x, rows, codes, scales, bad);
+    else if (vec && (reinterpret_cast<uintptr_t>(codes) % 16 == 0) && cols == 256)
+        quantize_rows8_kernel<8><<<blocks8, threads, 0, stream>>>(x, rows, codes, scales, bad);
+    else if (vec && cols <= 128)
         quantize_rows_vec_kernel<1><<<blocks, threads, 0, stream>>>(x, rows, cols, codes, scales, bad);
     else if (vec && cols <= 256)
         quantize_rows_vec_kernel<2><<<blocks, threads, 0, stream>>>(x, rows, cols, codes, scales, bad);
@@ -215,6 +381,11 @@ cudaError_t launch_quantize_per_tensor(const float* x, int64_t slices, int64_t r
     const int64_t elems = rows * cols;
     const int vec = (elems % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
                     (reinterpret_cast<uintptr_t>(codes) % 4 == 0);
+    if (vec && elems % 16 == 0 && slices * kSliceCluster <= INT32_MAX) {
+        slice_quantize_fused_kernel<<<static_cast<unsigned>(slices * kSliceCluster), 512, 0,
+                                      stream>>>(x, elems, codes, slice_scales, bad);
+        return cudaGetLastError();
+    }
     cudaError_t err = cudaMemsetAsync(amax_ws, 0, sizeof(uint32_t) * slices, stream);
     if (err != cudaSuccess) return err;
     const int threads = 256;

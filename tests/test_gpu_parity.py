@@ -72,6 +72,69 @@ def test_quantize_per_tensor_bitwise(ifa, oracle, slices, rows, cols):
         assert _bits(got.scale[s].cpu().numpy()) == _bits(ws)
 
 
+def _boundary_rows(rows, cols, seed):
+    """Rows whose quotients x/scale sit on and one ulp around half-integers,
+    where a reciprocal-multiply estimate and the IEEE quotient can round
+    differently (the kernels must take their exact path there)."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((rows, cols)).astype(np.float32)
+    for r in range(rows):
+        m = np.float32(abs(x[r]).max())
+        x[r, 0] = m if r % 2 else -m
+        scale = np.float32(m / np.float32(127.0))
+        k = rng.integers(-126, 126, size=cols - 1).astype(np.float32) + np.float32(0.5)
+        mid = (k * scale).astype(np.float32)
+        step = rng.integers(-2, 3, size=cols - 1)
+        vals = mid.copy()
+        up, dn = step > 0, step < 0
+        vals[up] = np.nextafter(mid[up], np.float32(np.inf))
+        vals[dn] = np.nextafter(mid[dn], np.float32(-np.inf))
+        vals[step == 2] = np.nextafter(vals[step == 2], np.float32(np.inf))
+        vals[step == -2] = np.nextafter(vals[step == -2], np.float32(-np.inf))
+        x[r, 1:] = np.clip(vals, -m, m)
+    return x
+
+
+@pytest.mark.parametrize("rows,cols", [(64, 128), (32, 64), (16, 256), (9, 100)])
+def test_quantize_rounding_boundaries_per_row(ifa, oracle, rows, cols):
+    x = _boundary_rows(rows, cols, seed=rows + cols)
+    want_c, want_s = oracle.quantize_per_row(x)
+    got = ifa.quantize_per_row(_dev(x))
+    assert np.array_equal(got.values.cpu().numpy(), want_c)
+    assert np.array_equal(_bits(got.scales.cpu().numpy()), _bits(want_s))
+
+
+@pytest.mark.parametrize("slices,rows,cols", [(3, 64, 128), (2, 16, 100)])
+def test_quantize_rounding_boundaries_per_tensor(ifa, oracle, slices, rows, cols):
+    x = np.stack([_boundary_rows(rows, cols, seed=s) for s in range(slices)])
+    for s in range(slices):   # one tensor scale per slice: rebuild around it
+        m = np.float32(abs(x[s]).max())
+        scale = np.float32(m / np.float32(127.0))
+        flat = x[s].reshape(-1)
+        k = np.round(flat[1:] / scale - 0.5).astype(np.float32) + np.float32(0.5)
+        flat[1:] = np.clip((k * scale).astype(np.float32), -m, m)
+        x[s] = flat.reshape(rows, cols)
+    got = ifa.quantize_per_tensor(_dev(x))
+    for s in range(slices):
+        wc, ws = oracle.quantize_per_tensor(x[s])
+        assert np.array_equal(got.values[s].cpu().numpy(), wc)
+        assert _bits(got.scale[s].cpu().numpy()) == _bits(ws)
+
+
+@pytest.mark.parametrize("shape,where", [((64, 128), (37, 5)), ((16, 256), (3, 200)),
+                                         ((4, 64, 128), (2, 60, 127))])
+def test_quantize_nonfinite_index_vectorised_paths(ifa, shape, where):
+    x = torch.randn(shape, device="cuda")
+    x[where] = float("nan")
+    flat = int(np.ravel_multi_index(where, shape))
+    fn = ifa.quantize_per_tensor if len(shape) == 3 else ifa.quantize_per_row
+    with pytest.raises(ValueError, match=f"index {flat}$"):
+        fn(x)
+    x[where] = float("inf")
+    with pytest.raises(ValueError, match=f"index {flat}$"):
+        fn(x)
+
+
 def test_quantize_rejects_nonfinite_with_index(ifa):
     x = torch.tensor([[1.0, 2.0], [float("inf"), 4.0]], device="cuda")
     with pytest.raises(ValueError, match="index 2"):
