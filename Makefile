@@ -24,8 +24,8 @@ $(LIB): $(SRCS) $(HDRS)
 oracle:
 	$(MAKE) -s -C oracle all
 
-ref:
-	$(MAKE) -s -C oracle ref refa
+ref: $(LIB)
+	$(MAKE) -s -C oracle ref refa verify
 
 sass: $(LIB)
 	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > $(PKG)/lib/sass.txt

@@ -17,6 +17,7 @@
 // for IFA_ENOTSUP / IFA_ECUDA (no CPU fallback exists).
 #pragma once
 
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 
@@ -37,8 +38,10 @@ inline void check(int rc) {
 /// Drop-in for ifa::quantize_per_row (quant.hpp:30, quant.cpp:44-57).
 inline ifa::QuantizedRows quantize_per_row(const ifa::FloatMatrix& m) {
     ifa::QuantizedRows out{ifa::Int8Matrix(m.rows(), m.cols()), ifa::ScaleVector(m.rows())};
+    if (m.rows() == 0) return out;
+    // ScaleVector exposes mutable storage through operator[] only
     check(ifa_quantize_per_row_host(m.data(), m.rows(), m.cols(), out.values.data(),
-                                    out.scales.data(), nullptr, nullptr));
+                                    &out.scales[0], nullptr, nullptr));
     return out;
 }
 
