@@ -287,6 +287,9 @@ def main() -> None:
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--dist", default="normal", choices=["normal", "uniform"],
                     help="synthetic activations: N(0,1) or U(-0.5,0.5) (eval.cpp:46-51)")
+    ap.add_argument("--mode", default="exact", choices=["exact", "fast"],
+                    help="exact: O bitwise equal to the reference; fast: tolerance mode "
+                         "(IFA_FLAG_FAST, O within MRE 5e-5 of the reference)")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip e2e / cpu baseline / fp16 / int8-peak probes")
     args = ap.parse_args()
@@ -330,7 +333,8 @@ def main() -> None:
         return torch.randn((slices, N, d), generator=gen, device=dev, dtype=torch.float32)
 
     q, k, v = synth(), synth(), synth()
-    plan = AttentionPlan(slices, N, d, bc=bc, br=128, causal=causal, device=dev)
+    plan = AttentionPlan(slices, N, d, bc=bc, br=128, causal=causal, fast=args.mode == "fast",
+                         device=dev)
 
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):

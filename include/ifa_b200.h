@@ -50,6 +50,13 @@ extern "C" {
 /* ifa_int_flash_fwd flags */
 #define IFA_FLAG_SQRT_D 1u /* AttentionConfig::apply_sqrt_d_scaling (attention.hpp:25-27) */
 #define IFA_FLAG_CAUSAL 2u /* extension (not in the reference): row i sees keys j <= i   */
+/* Tolerance mode: the same per-block algorithm (Bc honoured, running-max
+ * requantization, per-block float rescale) with one MUFU exp2 per code and no
+ * exactness guard.  int8 codes, scales and int32 S are unaffected; O agrees
+ * with the reference within the tolerance tests/test_gpu_parity.py states
+ * (MRE <= 5e-5, max|dO| <= the reference's multi-block bound 2/127*max|V|*sV,
+ * verify.cpp:65-70).  Ignored when an audit is requested. */
+#define IFA_FLAG_FAST 4u
 
 /* Device-resident mirror of ifa::PCodeAudit (attention.hpp:75-80).  Before
  * a call the struct must hold {127, 0, 1, 0, 0} (ifa_audit_init()); the

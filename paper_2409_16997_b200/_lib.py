@@ -19,6 +19,7 @@ IFA_ECUDA = 1000
 
 FLAG_SQRT_D = 1
 FLAG_CAUSAL = 2
+FLAG_FAST = 4
 
 # Every symbol include/ifa_b200.h declares.
 EXPORTED_SYMBOLS = (

@@ -85,6 +85,9 @@ class AttentionConfig:
     blocks: BlockSpec = field(default_factory=BlockSpec)
     apply_sqrt_d_scaling: bool = False
     causal: bool = False
+    # tolerance mode (IFA_FLAG_FAST): O within the stated tolerance instead of
+    # bitwise; codes, scales and S stay exact
+    fast: bool = False
 
     def validate(self) -> None:
         self.blocks.validate()
@@ -213,7 +216,7 @@ def int_flash_attention(inputs: QuantizedAttentionInputs,
     if out is None:
         out = torch.empty(qv.shape, dtype=torch.float32, device=qv.device)
     flags = (_lib.FLAG_SQRT_D if cfg.apply_sqrt_d_scaling else 0) | \
-        (_lib.FLAG_CAUSAL if cfg.causal else 0)
+        (_lib.FLAG_CAUSAL if cfg.causal else 0) | (_lib.FLAG_FAST if cfg.fast else 0)
     lib = _lib.load()
     au = None
     sp = _stream_ptr(stream)

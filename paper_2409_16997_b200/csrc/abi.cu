@@ -71,7 +71,7 @@ int validate_fwd(int64_t slices, int64_t n, int64_t d, int64_t br, int64_t bc, u
     if (kv_depth > IFA_MAX_INT_GEMM_DEPTH)
         return fail(IFA_EOVERFLOW, "int gemm depth " + std::to_string(kv_depth) +
                                        " exceeds 133144; int32 accumulation could overflow");
-    if (flags & ~(IFA_FLAG_SQRT_D | IFA_FLAG_CAUSAL))
+    if (flags & ~(IFA_FLAG_SQRT_D | IFA_FLAG_CAUSAL | IFA_FLAG_FAST))
         return fail(IFA_EINVAL, "int_flash_attention: unknown flag bits");
     if (d > 128)
         return fail(IFA_ENOTSUP, "int_flash_attention: head dim " + std::to_string(d) +

@@ -92,6 +92,7 @@ constexpr float kMagic = 12582912.0f;       // 1.5 * 2^23: rounds to the nearest
 // boundary (a half-integer) are settled exactly (code_bounds.h).
 constexpr float kGuardBase = 1.3e-4f;
 constexpr float kGuardScale = 5.5e-6f;
+constexpr int kGuardGroup = 16;  // codes checked per branch
 
 enum ItemKind : uint32_t {
     K_MAXONLY = 1u,   // pass-1 sub-tile of a multi-tile block: contributes to the row max
@@ -152,6 +153,39 @@ struct ItemGen {
     }
 };
 
+// Fast-path item sequence (Bc == 128 or Bc == n <= 128, non-causal): one
+// full block per tile.
+struct TileGen {
+    int32_t n;
+    int32_t key0 = 0;
+    __device__ explicit TileGen(int32_t n_) : n(n_) {}
+    __device__ __forceinline__ bool next(Item& it) {
+        if (key0 >= n) return false;
+        it.key0 = key0;
+        it.width = n - key0 < BN ? n - key0 : BN;
+        it.kind = K_BEGIN | K_MAXDONE | K_PV | K_PV_FIRST | K_END;
+        key0 += BN;
+        return true;
+    }
+};
+
+template <bool GENERIC>
+struct GenOf {
+    using type = ItemGen;
+};
+template <>
+struct GenOf<false> {
+    using type = TileGen;
+};
+template <bool GENERIC>
+__device__ __forceinline__ typename GenOf<GENERIC>::type make_gen(int32_t n, int32_t bc,
+                                                                  int32_t kv_limit) {
+    if constexpr (GENERIC)
+        return ItemGen(n, bc, kv_limit);
+    else
+        return TileGen(n);
+}
+
 template <int D>
 struct alignas(1024) Smem {
     uint8_t q[2][BM * D];
@@ -160,6 +194,7 @@ struct alignas(1024) Smem {
     uint8_t ones[16 * BN];  // all-ones B tile: P . 1 = exact int32 row sum of the codes
     float sk[STAGES][BN];
     float xmax[2][SPLIT][BM];  // [item parity][part][row]: partial row max exchange
+    float alpha[2][BM];        // [block parity][row]: expf(m - m_new), computed by one part
     float bounds[128];         // B[k]: exact code decision boundaries (code_bounds.h)
     uint64_t q_full[2], q_empty[2];
     uint64_t k_full[STAGES], v_full[STAGES], kv_empty[STAGES];
@@ -215,7 +250,7 @@ __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 // (int)round(127*expf(s - m_new)), packed 4 per word.  Fast path: y =
 // ex2(s*log2e + c_r) with c_r = log2(127) - m_new*log2e, rounded by the
 // magic-number add; every element also measures its distance to that
-// integer.  Only when an estimate of a group of 8 lies within the guard band
+// integer.  Only when an estimate of a group of kGuardGroup lies within the guard band
 // of a rounding boundary k+1/2 (rare) are the ambiguous codes settled exactly by
 // one comparison against the precomputed boundary B[k] of the reference's
 // code function (code_bounds.h).
@@ -224,10 +259,10 @@ __device__ __forceinline__ void codes_part(const float (&s)[NCOL], float m_new, 
                                            uint32_t (&w)[NCOL / 4]) {
     const float2 c2 = f2(c_r);
 #pragma unroll
-    for (int g0 = 0; g0 < NCOL; g0 += 8) {
-        float df[8];
+    for (int g0 = 0; g0 < NCOL; g0 += kGuardGroup) {
+        float df[kGuardGroup];
 #pragma unroll
-        for (int c = g0; c < g0 + 8; c += 4) {
+        for (int c = g0; c < g0 + kGuardGroup; c += 4) {
             const float2 ta = ffma2(make_float2(s[c], s[c + 1]), f2(kLog2e), c2);
             const float2 tb = ffma2(make_float2(s[c + 2], s[c + 3]), f2(kLog2e), c2);
             const float2 ya = make_float2(ex2_approx(ta.x), ex2_approx(ta.y));
@@ -244,12 +279,12 @@ __device__ __forceinline__ void codes_part(const float (&s)[NCOL], float m_new, 
                                     __byte_perm(__float_as_uint(rb.x), __float_as_uint(rb.y), 0x0040),
                                     0x5410);
         }
-        const float g = fmaxf(fmax3(fmax3(fabsf(df[0]), fabsf(df[1]), fabsf(df[2])),
-                                    fmax3(fabsf(df[3]), fabsf(df[4]), fabsf(df[5])), fabsf(df[6])),
-                              fabsf(df[7]));
+        float g = 0.0f;
+#pragma unroll
+        for (int e = 0; e < kGuardGroup; e += 2) g = fmax3(g, fabsf(df[e]), fabsf(df[e + 1]));
         if (g > thresh) {  // rare: settle the ambiguous codes exactly
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
+            for (int e = 0; e < kGuardGroup; ++e) {
                 if (fabsf(df[e]) > thresh) {
                     const int c = g0 + e;
                     const uint32_t sh = 8u * (c & 3);
@@ -260,6 +295,23 @@ __device__ __forceinline__ void codes_part(const float (&s)[NCOL], float m_new, 
                 }
             }
         }
+    }
+}
+
+// Tolerance mode (IFA_FLAG_FAST): u are log2-domain scores; the code is
+// rint(2^(u - m + log2 127)) from one MUFU estimate (no exactness guard).
+__device__ __forceinline__ void codes_fast(const float (&u)[NCOL], float c_r,
+                                           uint32_t (&w)[NCOL / 4]) {
+    const float2 c2 = f2(c_r);
+#pragma unroll
+    for (int c = 0; c < NCOL; c += 4) {
+        const float2 ta = fadd2(make_float2(u[c], u[c + 1]), c2);
+        const float2 tb = fadd2(make_float2(u[c + 2], u[c + 3]), c2);
+        const float2 ra = fadd2(make_float2(ex2_approx(ta.x), ex2_approx(ta.y)), f2(kMagic));
+        const float2 rb = fadd2(make_float2(ex2_approx(tb.x), ex2_approx(tb.y)), f2(kMagic));
+        w[c >> 2] = __byte_perm(__byte_perm(__float_as_uint(ra.x), __float_as_uint(ra.y), 0x0040),
+                                __byte_perm(__float_as_uint(rb.x), __float_as_uint(rb.y), 0x0040),
+                                0x5410);
     }
 }
 
@@ -287,9 +339,10 @@ struct Ring {
     }
 };
 
-// GENERIC = false: the benchmark-shaped fast path (non-causal, Bc <= 128,
-// no audit, no 1/sqrt(d)); true: every feature, selected at run time.
-template <int D, bool GENERIC>
+// GENERIC = false: the benchmark-shaped fast path (non-causal, KV blocks
+// equal to the 128-key tiles, no audit, no 1/sqrt(d)); true: every feature,
+// selected at run time.
+template <int D, bool GENERIC, bool FAST>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     int_flash_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_k,
@@ -371,7 +424,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 tma_load_3d(sm.q[qb], &tm_q, &sm.q_full[qb], 0, w.q0, w.slice, pol_stream);
             }
             const float* sk_slice = p.sk + static_cast<int64_t>(w.slice) * n;
-            ItemGen gen(n, p.bc, w.kv_limit);
+            auto gen = make_gen<GENERIC>(n, p.bc, w.kv_limit);
             Item it;
             while (gen.next(it)) {
                 const uint32_t st = kv.idx;
@@ -444,7 +497,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 bar_wait(b_q_full + 8 * qb, (wi >> 1) & 1);
                 tc_fence_after();
                 const uint32_t q_base = smem_u32(sm.q[qb]);
-                ItemGen gen(n, p.bc, w.kv_limit);
+                auto gen = make_gen<GENERIC>(n, p.bc, w.kv_limit);
                 Item it;
                 while (gen.next(it)) {
                     const uint32_t st = kv.idx;
@@ -510,6 +563,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int32_t grow = w.q0 + row;
             const bool row_ok = grow < n;
             const float sq_r = row_ok ? p.sq[static_cast<int64_t>(w.slice) * n + grow] : 0.0f;
+            const float bq_r = sq_r * kLog2e * (use_extra ? extra : 1.0f);  // FAST only
             float acc[NCOL];
 #pragma unroll
             for (int c = 0; c < NCOL; ++c) acc[c] = 0.0f;
@@ -518,10 +572,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             float blk_max = kNegInf, m_new = kNegInf;
             bool has_full = false, row_hit = false;
             bool pend = false;
-            float pend_alpha = 1.0f;
+            float pend_alpha = 1.0f;  // FAST: computed by every thread
 
             // acc = acc*alpha + float(PV), l = l*alpha + float(rowsum)
-            // (attention.cpp:313-318, :330-333) for the finished block bi.
+            // (attention.cpp:313-318, :330-333) for the finished block bi;
+            // alpha was published in SMEM by the block's designated part.
             auto fold_pv = [&](float alpha) {
                 bar_wait(b_pv_full, bi & 1);
                 tc_fence_after();
@@ -536,6 +591,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 __syncwarp();
                 if (lane == 0) bar_arrive(b_pv_empty);
                 ++bi;
+                if constexpr (FAST) {
+                    l = __fmaf_rn(l, alpha, static_cast<float>(static_cast<int32_t>(rs)));
+#pragma unroll
+                    for (int c = 0; c < NCOL; c += 2) {
+                        const float2 pf = make_float2(__int2float_rn(static_cast<int32_t>(pv[c])),
+                                                      __int2float_rn(static_cast<int32_t>(pv[c + 1])));
+                        const float2 a = ffma2(make_float2(acc[c], acc[c + 1]), f2(alpha), pf);
+                        acc[c] = a.x;
+                        acc[c + 1] = a.y;
+                    }
+                    return;
+                }
                 l = __fadd_rn(__fmul_rn(l, alpha), static_cast<float>(static_cast<int32_t>(rs)));
                 // acc *= alpha, rounded before the add (no FMA); skipped when
                 // alpha == 1 for the whole warp, which leaves acc bit-identical.
@@ -559,7 +626,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
             };
 
-            ItemGen gen(n, p.bc, w.kv_limit);
+            auto gen = make_gen<GENERIC>(n, p.bc, w.kv_limit);
             Item it;
             while (gen.next(it)) {
                 const uint32_t st = kv.idx;
@@ -579,9 +646,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     if (vis < lim) lim = vis < 0 ? 0 : vis;
                 }
                 lim -= c_base;  // columns of this slice still visible
-                // dequantize: s = float(S) * (sQ * sK) [* extra], product of scales first
                 float s[NCOL];
                 const float4* sk4 = reinterpret_cast<const float4*>(sk_part + st * BN);
+                if constexpr (FAST) {
+                    // log2-domain scores u = float(S) * (sQ*log2e[*extra] * sK)
+#pragma unroll
+                    for (int c4 = 0; c4 < NCOL / 4; ++c4) {
+                        const float4 k4 = sk4[c4];
+                        const int c = c4 * 4;
+                        const float2 sf01 = make_float2(__int2float_rn(static_cast<int32_t>(sr[c])),
+                                                        __int2float_rn(static_cast<int32_t>(sr[c + 1])));
+                        const float2 sf23 = make_float2(__int2float_rn(static_cast<int32_t>(sr[c + 2])),
+                                                        __int2float_rn(static_cast<int32_t>(sr[c + 3])));
+                        const float2 s01 = fmul2(sf01, fmul2(f2(bq_r), make_float2(k4.x, k4.y)));
+                        const float2 s23 = fmul2(sf23, fmul2(f2(bq_r), make_float2(k4.z, k4.w)));
+                        s[c] = s01.x;
+                        s[c + 1] = s01.y;
+                        s[c + 2] = s23.x;
+                        s[c + 3] = s23.y;
+                    }
+                } else {
+                // dequantize: s = float(S) * (sQ * sK) [* extra], product of scales first
 #pragma unroll
                 for (int c4 = 0; c4 < NCOL / 4; ++c4) {
                     const float4 k4 = sk4[c4];
@@ -601,6 +686,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     s[c + 1] = s01.y;
                     s[c + 2] = s23.x;
                     s[c + 3] = s23.y;
+                }
                 }
                 __syncwarp();
                 if (lane == 0) bar_arrive(b_kv_empty + 8 * st);
@@ -640,11 +726,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         tc_fence_after();
                     }
                     uint32_t wd[NCOL / 4];
-                    const float mL = __fmul_rn(m_new, kLog2e);
-                    const float c_r = __fsub_rn(kLog2_127, mL);
-                    const float thresh =
-                        0.5f - (kGuardBase + kGuardScale * (fabsf(mL) + fabsf(c_r)));
-                    codes_part(s, m_new, c_r, thresh, sm.bounds, wd);
+                    if constexpr (FAST) {
+                        codes_fast(s, kLog2_127 - m_new, wd);
+                    } else {
+                        const float mL = __fmul_rn(m_new, kLog2e);
+                        const float c_r = __fsub_rn(kLog2_127, mL);
+                        const float thresh =
+                            0.5f - (kGuardBase + kGuardScale * (fabsf(mL) + fabsf(c_r)));
+                        codes_part(s, m_new, c_r, thresh, sm.bounds, wd);
+                    }
                     asm volatile(
                         "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
                             t_p + 32 * (pi & 1)),
@@ -659,7 +749,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     // the code stores drain; it must precede p_full so the
                     // next P.V may overwrite the single accumulator
                     if (pend) {
-                        fold_pv(pend_alpha);
+                        fold_pv(FAST ? pend_alpha : sm.alpha[bi & 1][row]);
                         pend = false;
                     }
                     tmem_wait_st();
@@ -668,21 +758,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     if (lane == 0) bar_arrive(b_p_full + 8 * (pi & 1));
                     ++pi;
                     if (it.kind & K_END) {
-                        // alpha = expf(m - m_new) (attention.cpp:298); exp(0) = 1
-                        const float alpha = (m_new == m) ? 1.0f : exact_expf(__fsub_rn(m, m_new));
+                        // alpha = expf(m - m_new) (attention.cpp:298), exp(0) = 1: one
+                        // part per block computes it (rotating) and publishes it;
+                        // the fold reads it after the next row-max barrier
+                        if constexpr (FAST) {
+                            pend_alpha = (m_new == m) ? 1.0f : ex2_approx(m - m_new);
+                        } else if (part == (bi & 3)) {
+                            const float alpha =
+                                (m_new == m) ? 1.0f : exact_expf(__fsub_rn(m, m_new));
+                            sm.alpha[bi & 1][row] = alpha;
+                        }
                         if (m_new > m)
                             row_hit = has_full;
                         else if (blk_max == m_new && has_full)
                             row_hit = true;
                         m = m_new;
                         pend = true;  // its P.V is folded during the next tile
-                        pend_alpha = alpha;
                     }
                 }
                 kv.advance();
                 ++i;
             }
-            if (pend) fold_pv(pend_alpha);
+            if (pend) {
+                if (!FAST) named_bar_sync(bar_id, 32 * SPLIT);  // the last alpha is published
+                fold_pv(FAST ? pend_alpha : sm.alpha[bi & 1][row]);
+            }
 
             // epilogue: O = (acc / l) * sV (attention.cpp:335-342)
             if (row_ok && c_base < p.d) {
@@ -691,7 +791,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 float* orow = p.o + (static_cast<int64_t>(w.slice) * n + grow) * d + c_base;
                 float out[NCOL];
 #pragma unroll
-                for (int c = 0; c < NCOL; ++c) out[c] = __fmul_rn(__fdiv_rn(acc[c], l), sv);
+                if constexpr (FAST) {
+                    const float f = __fdiv_rn(sv, l);
+#pragma unroll
+                    for (int c = 0; c < NCOL; ++c) out[c] = acc[c] * f;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < NCOL; ++c) out[c] = __fmul_rn(__fdiv_rn(acc[c], l), sv);
+                }
                 if (d % 4 == 0 && c_base + NCOL <= d) {
 #pragma unroll
                     for (int c = 0; c < NCOL; c += 4)
@@ -778,13 +885,13 @@ static bool make_map(CUtensorMap* map, const int8_t* base, int64_t slices, int64
     return r == CUDA_SUCCESS;
 }
 
-template <int D, bool GENERIC>
+template <int D, bool GENERIC, bool FAST>
 static cudaError_t launch_k(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                             const Params& p, int64_t slices, cudaStream_t stream) {
     const size_t smem = sizeof(Smem<D>) + 1024;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(int_flash_fwd_kernel<D, GENERIC>,
+        cudaError_t e = cudaFuncSetAttribute(int_flash_fwd_kernel<D, GENERIC, FAST>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
@@ -801,7 +908,7 @@ static cudaError_t launch_k(const CUtensorMap& tq, const CUtensorMap& tk, const 
     }
     (void)slices;
     const int grid = p.items < sms ? p.items : sms;
-    int_flash_fwd_kernel<D, GENERIC><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+    int_flash_fwd_kernel<D, GENERIC, FAST><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
     return cudaGetLastError();
 }
 
@@ -829,10 +936,17 @@ static cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
     const float* bounds = code_bounds();
     for (int k = 0; k < 128; ++k) p.bounds[k] = bounds[k];
     // the benchmark-shaped fast path, or the fully general kernel
+    // (fast path: every KV block is exactly one 128-key tile, or the whole
+    // sequence when it is shorter)
+    const bool tiles_are_blocks = p.bc == BN || (p.bc == p.n && p.n <= BN);
     const bool generic = a.audit != nullptr || (a.flags & (IFA_FLAG_SQRT_D | IFA_FLAG_CAUSAL)) ||
-                         p.bc > BN;
-    return generic ? launch_k<D, true>(tq, tk, tv, p, a.slices, stream)
-                   : launch_k<D, false>(tq, tk, tv, p, a.slices, stream);
+                         !tiles_are_blocks;
+    // tolerance mode (no audit: the audit reports the exact codes)
+    if ((a.flags & IFA_FLAG_FAST) && a.audit == nullptr)
+        return generic ? launch_k<D, true, true>(tq, tk, tv, p, a.slices, stream)
+                       : launch_k<D, false, true>(tq, tk, tv, p, a.slices, stream);
+    return generic ? launch_k<D, true, false>(tq, tk, tv, p, a.slices, stream)
+                   : launch_k<D, false, false>(tq, tk, tv, p, a.slices, stream);
 }
 
 }  // namespace attn

@@ -23,7 +23,7 @@ _INT64_MAX = (1 << 63) - 1
 
 class AttentionPlan:
     def __init__(self, slices: int, n: int, d: int, *, bc: int = 128, br: int = 128,
-                 causal: bool = False, sqrt_d: bool = False,
+                 causal: bool = False, sqrt_d: bool = False, fast: bool = False,
                  device: Optional[torch.device] = None):
         if slices < 1 or n < 1 or d < 1:
             raise ValueError("AttentionPlan: slices, n and d must be >= 1")
@@ -33,7 +33,8 @@ class AttentionPlan:
         dev = torch.device(device) if device is not None else torch.device("cuda")
         self.device = dev
         self.slices, self.n, self.d, self.bc, self.br = slices, n, d, bc, br
-        self.flags = (_lib.FLAG_CAUSAL if causal else 0) | (_lib.FLAG_SQRT_D if sqrt_d else 0)
+        self.flags = (_lib.FLAG_CAUSAL if causal else 0) | (_lib.FLAG_SQRT_D if sqrt_d else 0) | \
+            (_lib.FLAG_FAST if fast else 0)
         shape = (slices, n, d)
         self.qc = torch.empty(shape, dtype=torch.int8, device=dev)
         self.kc = torch.empty(shape, dtype=torch.int8, device=dev)

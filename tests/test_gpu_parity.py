@@ -241,3 +241,51 @@ def test_validation_errors(ifa):
         ifa.int_flash_attention(bad_v)
     with pytest.raises(ValueError):
         ifa.int_flash_attention(good, ifa.AttentionConfig(ifa.BlockSpec(0, 4)))
+
+
+# ---------------------------------------------------------------- tolerance mode
+# IFA_FLAG_FAST: same per-block algorithm, one MUFU exp2 per code, no
+# exactness guard.  Codes/scales/S are exact by construction (same quantize
+# kernels, same integer GEMM); O is held to the stated tolerance against the
+# exact reference result:
+#   MRE (normalized L1, eval.cpp:55-75) <= 5e-5, and
+#   max|dO| <= 2/127 * max|V_code| * sV   (the reference's own multi-block
+#   bound, verify.cpp:65-70).
+FAST_MRE = 5e-5
+
+
+def _fast_close(got, want, vc, vs):
+    bound = 2.0 / 127.0 * float(np.abs(vc).max()) * float(np.max(vs))
+    mre = float(np.abs(got.astype(np.float64) - want).sum() / max(np.abs(want).sum(), 1e-300))
+    return mre, float(np.abs(got.astype(np.float64) - want).max()), bound
+
+
+@pytest.mark.parametrize("n,d", [(1, 1), (24, 16), (128, 128), (300, 100), (1000, 128),
+                                 (4096, 128)])
+@pytest.mark.parametrize("dist", ["normal", "uniform"])
+@pytest.mark.parametrize("causal", [False, True])
+def test_fast_mode_within_tolerance(ifa, oracle, n, d, dist, causal):
+    _, (qc, qs, kc, ks, vc, vs) = _quantized_case(oracle, dist, n, d, seed=n + d)
+    want = oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, 128,
+                                      flags=2 if causal else 0)
+    inputs = ifa.QuantizedAttentionInputs(
+        ifa.QuantizedRows(_dev(qc), _dev(qs)), ifa.QuantizedRows(_dev(kc), _dev(ks)),
+        ifa.QuantizedTensor(_dev(vc), _dev(np.asarray(vs, np.float32))))
+    got = ifa.int_flash_attention(inputs, ifa.AttentionConfig(
+        ifa.BlockSpec(64, 128), causal=causal, fast=True)).cpu().numpy()
+    mre, mx, bound = _fast_close(got, want, vc, vs)
+    assert mre <= FAST_MRE, (mre, mx)
+    assert mx <= bound, (mre, mx, bound)
+
+
+@pytest.mark.parametrize("n,d,bc", [(40, 8, 3), (600, 128, 300), (257, 64, 200)])
+def test_fast_mode_odd_blocks(ifa, oracle, n, d, bc):
+    _, (qc, qs, kc, ks, vc, vs) = _quantized_case(oracle, "uniform", n, d, seed=bc)
+    want = oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, bc)
+    inputs = ifa.QuantizedAttentionInputs(
+        ifa.QuantizedRows(_dev(qc), _dev(qs)), ifa.QuantizedRows(_dev(kc), _dev(ks)),
+        ifa.QuantizedTensor(_dev(vc), _dev(np.asarray(vs, np.float32))))
+    got = ifa.int_flash_attention(inputs, ifa.AttentionConfig(
+        ifa.BlockSpec(64, bc), fast=True)).cpu().numpy()
+    mre, mx, bound = _fast_close(got, want, vc, vs)
+    assert mre <= FAST_MRE and mx <= bound, (mre, mx, bound)
