@@ -298,20 +298,48 @@ __device__ __forceinline__ void codes_part(const float (&s)[NCOL], float m_new, 
     }
 }
 
+// 2^t for a pair on the FMA pipe (tolerance mode): t = j + f, |f| <= 1/2,
+// degree-5 polynomial for 2^f (max rel. error 3.5e-7, i.e. < 5e-5 absolute
+// on a code <= 127), 2^j added to the exponent bits.  t is clamped at -64
+// (any t < -1 gives code 0).  Offloads part of the exp2 work from the MUFU
+// unit, which otherwise bounds the requantization phase.
+__device__ __forceinline__ float2 exp2_poly2(float2 t) {
+    t.x = fmaxf(t.x, -64.0f);
+    t.y = fmaxf(t.y, -64.0f);
+    const float2 r = fadd2(t, f2(kMagic));           // nearest integer j in the low bits
+    const float2 f = fsub2(t, fsub2(r, f2(kMagic)));  // t - j in [-1/2, 1/2]
+    float2 y = ffma2(f, f2(1.2915651313960552e-3f), f2(9.668535552918911e-3f));
+    y = ffma2(y, f, f2(5.5516887456178665e-2f));
+    y = ffma2(y, f, f2(2.4022264778614044e-1f));
+    y = ffma2(y, f, f2(6.931464672088623e-1f));
+    y = ffma2(y, f, f2(1.0f));
+    // bits(r) << 23 == j << 23 (the magic's own bits shift out)
+    return make_float2(__int_as_float(__float_as_int(y.x) + (__float_as_int(r.x) << 23)),
+                       __int_as_float(__float_as_int(y.y) + (__float_as_int(r.y) << 23)));
+}
+
 // Tolerance mode (IFA_FLAG_FAST): u are log2-domain scores; the code is
-// rint(2^(u - m + log2 127)) from one MUFU estimate (no exactness guard).
+// rint(2^(u - m + log2 127)), no exactness guard.  Per 8 codes, 6 exp2 run
+// on the MUFU unit and 2 on the FMA pipe.
 __device__ __forceinline__ void codes_fast(const float (&u)[NCOL], float c_r,
                                            uint32_t (&w)[NCOL / 4]) {
     const float2 c2 = f2(c_r);
 #pragma unroll
-    for (int c = 0; c < NCOL; c += 4) {
+    for (int c = 0; c < NCOL; c += 8) {
         const float2 ta = fadd2(make_float2(u[c], u[c + 1]), c2);
         const float2 tb = fadd2(make_float2(u[c + 2], u[c + 3]), c2);
+        const float2 tc = fadd2(make_float2(u[c + 4], u[c + 5]), c2);
+        const float2 td = fadd2(make_float2(u[c + 6], u[c + 7]), c2);
         const float2 ra = fadd2(make_float2(ex2_approx(ta.x), ex2_approx(ta.y)), f2(kMagic));
         const float2 rb = fadd2(make_float2(ex2_approx(tb.x), ex2_approx(tb.y)), f2(kMagic));
+        const float2 rc = fadd2(make_float2(ex2_approx(tc.x), ex2_approx(tc.y)), f2(kMagic));
+        const float2 rd = fadd2(exp2_poly2(td), f2(kMagic));
         w[c >> 2] = __byte_perm(__byte_perm(__float_as_uint(ra.x), __float_as_uint(ra.y), 0x0040),
                                 __byte_perm(__float_as_uint(rb.x), __float_as_uint(rb.y), 0x0040),
                                 0x5410);
+        w[(c >> 2) + 1] =
+            __byte_perm(__byte_perm(__float_as_uint(rc.x), __float_as_uint(rc.y), 0x0040),
+                        __byte_perm(__float_as_uint(rd.x), __float_as_uint(rd.y), 0x0040), 0x5410);
     }
 }
 
