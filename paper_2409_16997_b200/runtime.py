@@ -82,6 +82,14 @@ class AttentionPlan:
         self.quantize(q, k, v, stream)
         return self.attention(stream)
 
+    def launches_per_step(self) -> int:
+        """Kernels one forward() launches (quantize: Q rows, K rows, fused V
+        slices -- or absmax + quantize + a memset on shapes the fused V
+        kernel does not take; attention: one persistent kernel)."""
+        elems = self.n * self.d
+        v_fused = elems % 16 == 0 and self.d % 4 == 0
+        return 2 + (1 if v_fused else 3) + 1
+
     def check(self) -> None:
         """Raise like the reference if any quantized input was non-finite."""
         idx = int(self.bad.item())
