@@ -267,71 +267,100 @@ __global__ void __launch_bounds__(256) quantize_rows8_kernel(const float* __rest
     }
 }
 
-// V: one cluster of kSliceCluster CTAs per slice.  Pass 1: partial abs max
-// of this CTA's chunk; the cluster combines the partials through DSMEM.
-// Pass 2: quantize the chunk (re-read, now L2-resident).
+// V: clusters of kSliceCluster CTAs, each cluster walking slices (persistent,
+// so the slices in flight stay L2-resident).  Pass 1: partial abs max of this
+// CTA's chunk; the cluster combines the partials through DSMEM.  Pass 2:
+// quantize the chunk, re-read from L2.
 constexpr int kSliceCluster = 8;
 __global__ void __cluster_dims__(kSliceCluster, 1, 1) __launch_bounds__(512)
-    slice_quantize_fused_kernel(const float* __restrict__ x, int64_t slice_elems,
-                                int8_t* __restrict__ codes, float* __restrict__ slice_scales,
-                                int64_t* bad) {
+    slice_quantize_fused_kernel(const float* __restrict__ x, int64_t slices,
+                                int64_t slice_elems, int8_t* __restrict__ codes,
+                                float* __restrict__ slice_scales, int64_t* bad) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     __shared__ float red[16];
-    __shared__ float part;
-    const int64_t slice = blockIdx.x / kSliceCluster;
+    __shared__ float part[2];  // by iteration parity: a peer may still read the last one
+    const int64_t nclusters = gridDim.x / kSliceCluster;
     const int rank = static_cast<int>(cluster.block_rank());
     const int64_t n4 = slice_elems >> 2;
     const int64_t per = (n4 + kSliceCluster - 1) / kSliceCluster;
     const int64_t lo = rank * per;
     const int64_t hi = lo + per < n4 ? lo + per : n4;
-    const float4* src = reinterpret_cast<const float4*>(x + slice * slice_elems);
-    float m = 0.0f;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const float4 v = src[i];
-        m = absmax_nan(absmax_nan(m, v.x, v.y), v.z, v.w);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const float other = __shfl_xor_sync(0xffffffffu, m, o);
-        asm("max.NaN.f32 %0, %0, %1;" : "+f"(m) : "f"(other));
-    }
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+    int it = 0;
+    for (int64_t slice = blockIdx.x / kSliceCluster; slice < slices; slice += nclusters, ++it) {
+        const float4* src = reinterpret_cast<const float4*>(x + slice * slice_elems);
+        float m = 0.0f;
+        {
+            // four loads in flight per thread
+            const int64_t stride = blockDim.x;
+            int64_t i = lo + threadIdx.x;
+            for (; i + 3 * stride < hi; i += 4 * stride) {
+                const float4 a = src[i], b = src[i + stride], c = src[i + 2 * stride],
+                             d = src[i + 3 * stride];
+                m = absmax_nan(absmax_nan(m, a.x, a.y), a.z, a.w);
+                m = absmax_nan(absmax_nan(m, b.x, b.y), b.z, b.w);
+                m = absmax_nan(absmax_nan(m, c.x, c.y), c.z, c.w);
+                m = absmax_nan(absmax_nan(m, d.x, d.y), d.z, d.w);
+            }
+            for (; i < hi; i += stride) {
+                const float4 v = src[i];
+                m = absmax_nan(absmax_nan(m, v.x, v.y), v.z, v.w);
+            }
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            const float other = __shfl_xor_sync(0xffffffffu, v, o);
-            asm("max.NaN.f32 %0, %0, %1;" : "+f"(v) : "f"(other));
+            const float other = __shfl_xor_sync(0xffffffffu, m, o);
+            asm("max.NaN.f32 %0, %0, %1;" : "+f"(m) : "f"(other));
         }
-        if (threadIdx.x == 0) part = v;
-    }
-    cluster.sync();
-    float sm = 0.0f;
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
 #pragma unroll
-    for (int r = 0; r < kSliceCluster; ++r) {
-        const float other = *cluster.map_shared_rank(&part, r);
-        asm("max.NaN.f32 %0, %0, %1;" : "+f"(sm) : "f"(other));
-    }
-    const float scale = __fdiv_rn(sm, 127.0f);
-    if (rank == 0 && threadIdx.x == 0) slice_scales[slice] = scale;
-    if (!(sm <= 3.402823466e38f) && !(part <= 3.402823466e38f)) {  // locate it exactly
-        for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-            const float4 v = src[i];
-            const int64_t base = slice * slice_elems + 4 * i;
-            note_nonfinite(v.x, base + 0, bad);
-            note_nonfinite(v.y, base + 1, bad);
-            note_nonfinite(v.z, base + 2, bad);
-            note_nonfinite(v.w, base + 3, bad);
+            for (int o = 16; o > 0; o >>= 1) {
+                const float other = __shfl_xor_sync(0xffffffffu, v, o);
+                asm("max.NaN.f32 %0, %0, %1;" : "+f"(v) : "f"(other));
+            }
+            if (threadIdx.x == 0) part[it & 1] = v;
         }
+        cluster.sync();
+        float smax = 0.0f;
+#pragma unroll
+        for (int r = 0; r < kSliceCluster; ++r) {
+            const float other = *cluster.map_shared_rank(&part[it & 1], r);
+            asm("max.NaN.f32 %0, %0, %1;" : "+f"(smax) : "f"(other));
+        }
+        const float scale = __fdiv_rn(smax, 127.0f);
+        if (rank == 0 && threadIdx.x == 0) slice_scales[slice] = scale;
+        if (!(smax <= 3.402823466e38f) && !(part[it & 1] <= 3.402823466e38f)) {
+            for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {  // locate it exactly
+                const float4 v = src[i];
+                const int64_t base = slice * slice_elems + 4 * i;
+                note_nonfinite(v.x, base + 0, bad);
+                note_nonfinite(v.y, base + 1, bad);
+                note_nonfinite(v.z, base + 2, bad);
+                note_nonfinite(v.w, base + 3, bad);
+            }
+        }
+        const float rcp = __frcp_rn(scale);
+        const bool exact_row = !(rcp <= 3.402823466e38f);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(codes + slice * slice_elems);
+        {
+            const int64_t stride = blockDim.x;
+            int64_t i = lo + threadIdx.x;
+            for (; i + 3 * stride < hi; i += 4 * stride) {
+                const float4 a = __ldcs(src + i), b = __ldcs(src + i + stride),
+                             c = __ldcs(src + i + 2 * stride), d = __ldcs(src + i + 3 * stride);
+                dst[i] = codes4(a, scale, rcp, exact_row);
+                dst[i + stride] = codes4(b, scale, rcp, exact_row);
+                dst[i + 2 * stride] = codes4(c, scale, rcp, exact_row);
+                dst[i + 3 * stride] = codes4(d, scale, rcp, exact_row);
+            }
+            for (; i < hi; i += stride) dst[i] = codes4(__ldcs(src + i), scale, rcp, exact_row);
+        }
+        __syncthreads();  // red[] reuse
     }
-    const float rcp = __frcp_rn(scale);
-    const bool exact_row = !(rcp <= 3.402823466e38f);
-    uint32_t* dst = reinterpret_cast<uint32_t*>(codes + slice * slice_elems);
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
-        dst[i] = codes4(__ldcs(src + i), scale, rcp, exact_row);
-    cluster.sync();  // keep this CTA's `part` alive until every peer has read it
+    cluster.sync();  // keep `part` alive until every peer has read it
 }
 
 // ------------------------------------------------------------------ launchers
@@ -382,8 +411,15 @@ cudaError_t launch_quantize_per_tensor(const float* x, int64_t slices, int64_t r
     const int vec = (elems % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
                     (reinterpret_cast<uintptr_t>(codes) % 4 == 0);
     if (vec && elems % 16 == 0 && slices * kSliceCluster <= INT32_MAX) {
-        slice_quantize_fused_kernel<<<static_cast<unsigned>(slices * kSliceCluster), 512, 0,
-                                      stream>>>(x, elems, codes, slice_scales, bad);
+        // clusters in flight: ~48 MB of slices (L2-resident for the second
+        // pass), but at least enough CTAs to cover every SM
+        const int64_t slice_bytes = elems * 4;
+        int64_t nclusters = (64ll << 20) / slice_bytes;
+        const int64_t min_clusters = (sm_count() + kSliceCluster - 1) / kSliceCluster + 1;
+        if (nclusters < min_clusters) nclusters = min_clusters;
+        if (nclusters > slices) nclusters = slices;
+        slice_quantize_fused_kernel<<<static_cast<unsigned>(nclusters * kSliceCluster), 512, 0,
+                                      stream>>>(x, slices, elems, codes, slice_scales, bad);
         return cudaGetLastError();
     }
     cudaError_t err = cudaMemsetAsync(amax_ws, 0, sizeof(uint32_t) * slices, stream);
