@@ -193,7 +193,7 @@ struct alignas(1024) Smem {
     uint8_t v[STAGES][BN * D];
     uint8_t ones[16 * BN];  // all-ones B tile: P . 1 = exact int32 row sum of the codes
     float sk[STAGES][BN];
-    float xmax[2][SPLIT][BM];  // [item parity][part][row]: partial row max exchange
+    float xmax[2][BM][SPLIT];  // [item parity][row][part]: partial row max exchange
     float alpha[2][BM];        // [block parity][row]: expf(m - m_new), computed by one part
     float bounds[128];         // B[k]: exact code decision boundaries (code_bounds.h)
     uint64_t q_full[2], q_empty[2];
@@ -215,6 +215,7 @@ struct Params {
     int32_t bc;  // clamped to n by the host (any Bc >= n is one block)
     uint32_t flags;
     float extra;  // 1/sqrt(d) when IFA_FLAG_SQRT_D, else 1
+    float sk_mul;  // FAST: K scales are staged pre-multiplied by log2(e) [* extra]
     int32_t q_tiles;
     int32_t slices;
     int32_t items;  // q_tiles * slices
@@ -321,15 +322,16 @@ __device__ __forceinline__ float2 exp2_poly2(float2 t) {
 // Tolerance mode (IFA_FLAG_FAST): u are log2-domain scores; the code is
 // rint(2^(u - m + log2 127)), no exactness guard.  Per 8 codes, 6 exp2 run
 // on the MUFU unit and 2 on the FMA pipe.
-__device__ __forceinline__ void codes_fast(const float (&u)[NCOL], float c_r,
+__device__ __forceinline__ void codes_fast(const float (&u)[NCOL], float sq, float c_r,
                                            uint32_t (&w)[NCOL / 4]) {
-    const float2 c2 = f2(c_r);
+    const float2 c2 = f2(c_r), q2 = f2(sq);
 #pragma unroll
     for (int c = 0; c < NCOL; c += 8) {
-        const float2 ta = fadd2(make_float2(u[c], u[c + 1]), c2);
-        const float2 tb = fadd2(make_float2(u[c + 2], u[c + 3]), c2);
-        const float2 tc = fadd2(make_float2(u[c + 4], u[c + 5]), c2);
-        const float2 td = fadd2(make_float2(u[c + 6], u[c + 7]), c2);
+        // t = sQ * u + (log2(127) - sQ * m)
+        const float2 ta = ffma2(make_float2(u[c], u[c + 1]), q2, c2);
+        const float2 tb = ffma2(make_float2(u[c + 2], u[c + 3]), q2, c2);
+        const float2 tc = ffma2(make_float2(u[c + 4], u[c + 5]), q2, c2);
+        const float2 td = ffma2(make_float2(u[c + 6], u[c + 7]), q2, c2);
         const float2 ra = fadd2(make_float2(ex2_approx(ta.x), ex2_approx(ta.y)), f2(kMagic));
         const float2 rb = fadd2(make_float2(ex2_approx(tb.x), ex2_approx(tb.y)), f2(kMagic));
         const float2 rc = fadd2(make_float2(ex2_approx(tc.x), ex2_approx(tc.y)), f2(kMagic));
@@ -467,6 +469,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     kv4.z = key + 2 < n ? sk_slice[key + 2] : 0.0f;
                     kv4.w = key + 3 < n ? sk_slice[key + 3] : 0.0f;
                 }
+                if constexpr (FAST) {
+                    kv4.x *= p.sk_mul;
+                    kv4.y *= p.sk_mul;
+                    kv4.z *= p.sk_mul;
+                    kv4.w *= p.sk_mul;
+                }
                 reinterpret_cast<float4*>(sm.sk[st])[lane] = kv4;
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&sm.k_full[st], kTileBytes);
@@ -577,8 +585,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t bar_id = 1 + quarter;
         const float extra = p.extra;
         const bool use_extra = GENERIC && (p.flags & IFA_FLAG_SQRT_D) != 0;
-        float* const xmax_mine = &sm.xmax[0][part][row];
-        const float* const xmax_row = &sm.xmax[0][0][row];
+        float* const xmax_mine = &sm.xmax[0][row][part];
+        const float* const xmax_row = &sm.xmax[0][row][0];
         const float* const sk_part = &sm.sk[0][c_base];
         int32_t cmin = 127, cmax = 0;
         bool all_hit = true;
@@ -591,7 +599,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int32_t grow = w.q0 + row;
             const bool row_ok = grow < n;
             const float sq_r = row_ok ? p.sq[static_cast<int64_t>(w.slice) * n + grow] : 0.0f;
-            const float bq_r = sq_r * kLog2e * (use_extra ? extra : 1.0f);  // FAST only
             float acc[NCOL];
 #pragma unroll
             for (int c = 0; c < NCOL; ++c) acc[c] = 0.0f;
@@ -677,7 +684,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 float s[NCOL];
                 const float4* sk4 = reinterpret_cast<const float4*>(sk_part + st * BN);
                 if constexpr (FAST) {
-                    // log2-domain scores u = float(S) * (sQ*log2e[*extra] * sK)
+                    // u = float(S) * (sK * log2e [* extra]): log2-domain scores
+                    // before the per-row factor sQ (>= 0, so the row max
+                    // commutes with it; it is applied inside the exp2 FMA)
 #pragma unroll
                     for (int c4 = 0; c4 < NCOL / 4; ++c4) {
                         const float4 k4 = sk4[c4];
@@ -686,8 +695,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                                         __int2float_rn(static_cast<int32_t>(sr[c + 1])));
                         const float2 sf23 = make_float2(__int2float_rn(static_cast<int32_t>(sr[c + 2])),
                                                         __int2float_rn(static_cast<int32_t>(sr[c + 3])));
-                        const float2 s01 = fmul2(sf01, fmul2(f2(bq_r), make_float2(k4.x, k4.y)));
-                        const float2 s23 = fmul2(sf23, fmul2(f2(bq_r), make_float2(k4.z, k4.w)));
+                        const float2 s01 = fmul2(sf01, make_float2(k4.x, k4.y));
+                        const float2 s23 = fmul2(sf23, make_float2(k4.z, k4.w));
                         s[c] = s01.x;
                         s[c + 1] = s01.y;
                         s[c + 2] = s23.x;
@@ -735,8 +744,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 named_bar_sync(bar_id, 32 * SPLIT);
                 float m_loc;
                 {
-                    const float* xr = xmax_row + (i & 1) * SPLIT * BM;
-                    m_loc = fmaxf(fmax3(xr[0], xr[BM], xr[2 * BM]), xr[3 * BM]);
+                    const float4 x4 =
+                        *reinterpret_cast<const float4*>(xmax_row + (i & 1) * SPLIT * BM);
+                    m_loc = fmaxf(fmax3(x4.x, x4.y, x4.z), x4.w);
                 }
 
                 if (it.kind & K_BEGIN) blk_max = kNegInf;
@@ -755,7 +765,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                     uint32_t wd[NCOL / 4];
                     if constexpr (FAST) {
-                        codes_fast(s, kLog2_127 - m_new, wd);
+                        codes_fast(s, sq_r, kLog2_127 - sq_r * m_new, wd);
+                        if (lim < NCOL) {  // masked keys: code 0 even when sQ == 0
+#pragma unroll
+                            for (int c = 0; c < NCOL; ++c)
+                                if (c >= lim) wd[c >> 2] &= ~(0xffu << (8 * (c & 3)));
+                        }
                     } else {
                         const float mL = __fmul_rn(m_new, kLog2e);
                         const float c_r = __fsub_rn(kLog2_127, mL);
@@ -790,7 +805,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         // part per block computes it (rotating) and publishes it;
                         // the fold reads it after the next row-max barrier
                         if constexpr (FAST) {
-                            pend_alpha = (m_new == m) ? 1.0f : ex2_approx(m - m_new);
+                            pend_alpha = (m_new == m) ? 1.0f
+                                         : (m == kNegInf ? 0.0f : ex2_approx(sq_r * (m - m_new)));
                         } else if (part == (bi & 3)) {
                             const float alpha =
                                 (m_new == m) ? 1.0f : exact_expf(__fsub_rn(m, m_new));
@@ -958,6 +974,7 @@ static cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
     p.bc = static_cast<int32_t>(a.bc < a.n ? a.bc : a.n);
     p.flags = a.flags;
     p.extra = (a.flags & IFA_FLAG_SQRT_D) ? 1.0f / sqrtf(static_cast<float>(a.d)) : 1.0f;
+    p.sk_mul = 1.4426950408889634f * p.extra;
     p.q_tiles = static_cast<int32_t>((a.n + BM - 1) / BM);
     p.slices = static_cast<int32_t>(a.slices);
     p.items = p.q_tiles * p.slices;
