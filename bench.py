@@ -307,10 +307,20 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # Test hook (not used by the driver): IFA_BENCH_SHARE_GPU=1 maps every
+    # rank onto the visible GPUs round-robin and IFA_BENCH_BACKEND=gloo
+    # swaps the timing/verification collectives to gloo, so the N>1 code
+    # path can be exercised on a one-GPU box.
+    if os.environ.get("IFA_BENCH_SHARE_GPU") == "1":
+        local = local % max(torch.cuda.device_count(), 1)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("IFA_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     from paper_2409_16997_b200.runtime import AttentionPlan
 

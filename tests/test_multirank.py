@@ -7,9 +7,12 @@ single-process run bit for bit.
 """
 import os
 import socket
+import sys
 
 import numpy as np
 import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _free_port():
@@ -65,3 +68,21 @@ def test_sharded_run_equals_single_process(tmp_path, oracle, total):
         vc, vs = oracle.quantize_per_tensor(v)
         want.append(oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, 32))
     assert np.array_equal(got.view(np.uint32), np.stack(want).view(np.uint32))
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_share_one_gpu(tmp_path):
+    """bench.py's N>1 path (torchrun, per-rank shards, max-over-ranks timing,
+    checksum gather) on a one-GPU box: both ranks share the GPU and the
+    collectives run on gloo (IFA_BENCH_SHARE_GPU / IFA_BENCH_BACKEND hooks)."""
+    import json
+    import subprocess
+    env = dict(os.environ, IFA_BENCH_SHARE_GPU="1", IFA_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--workload", "c5", "--steps", "1", "--warmup", "3", "--no-extras"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and len(line["checksums"]) == 2
+    assert line["config"]["slices_per_rank"] == 1024 and line["scaling"] == "strong"
