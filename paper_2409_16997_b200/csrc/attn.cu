@@ -52,6 +52,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "code_bounds.h"
 #include "exact_expf.cuh"
@@ -77,6 +78,10 @@ constexpr int NUM_THREADS = 32 * (SOFT_WARP0 + SOFT_WARPS);
 constexpr uint32_t kRegsControl = 32;
 constexpr uint32_t kRegsSoftmax = 112;
 static_assert(kRegsControl + 4 * kRegsSoftmax <= 5 * 96, "register budget");
+// quad kernels: 12 warps launch at 168 registers; per sub-partition one
+// control warp (32) and two math warps (232): 32 + 2*232 <= 3*168
+constexpr uint32_t kRegsControlQuad = 32;
+constexpr uint32_t kRegsMathQuad = 232;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t T_S = 0, T_PV = 128, T_RS = 256, T_P0 = 288;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -156,11 +161,11 @@ struct ItemGen {
 // Fast-path item sequence (Bc == 128 or Bc == n <= 128, non-causal): one
 // full block per tile.
 struct TileGen {
-    int32_t n;
+    int32_t n, kv_limit;
     int32_t key0 = 0;
-    __device__ explicit TileGen(int32_t n_) : n(n_) {}
+    __device__ TileGen(int32_t n_, int32_t kv_limit_) : n(n_), kv_limit(kv_limit_) {}
     __device__ __forceinline__ bool next(Item& it) {
-        if (key0 >= n) return false;
+        if (key0 >= kv_limit) return false;
         it.key0 = key0;
         it.width = n - key0 < BN ? n - key0 : BN;
         it.kind = K_BEGIN | K_MAXDONE | K_PV | K_PV_FIRST | K_END;
@@ -183,7 +188,7 @@ __device__ __forceinline__ typename GenOf<GENERIC>::type make_gen(int32_t n, int
     if constexpr (GENERIC)
         return ItemGen(n, bc, kv_limit);
     else
-        return TileGen(n);
+        return TileGen(n, kv_limit);
 }
 
 template <int D>
@@ -369,14 +374,307 @@ struct Ring {
     }
 };
 
+// ----------------------------------------------------------------------------
+// Quad layout (QUAD kernels, 8 math warps): the 16x256b TMEM shape gives the
+// four threads of a quad two rows (r, r+8) and 32 of their 128 columns, so a
+// row's maximum is combined with two shuffles -- no cross-warp barrier, and
+// half the per-tile fixed costs of the 16-warp layout.  The V tile is
+// loaded with its rows permuted inside each 32-key group (see
+// make_map_vperm) so each thread's packed codes land in whole 32-bit P
+// words.
+constexpr int QUAD_WARPS = 8;
+
+template <int N>
+__device__ __forceinline__ void tmem_ld_16x256b(uint32_t taddr, uint32_t (&r)[N]);
+template <>
+__device__ __forceinline__ void tmem_ld_16x256b<16>(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+template <>
+__device__ __forceinline__ void tmem_ld_16x256b<4>(uint32_t taddr, uint32_t (&r)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st_16x256b_x4(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+        "r"(r[15])
+        : "memory");
+}
+
+// Two values of one row -> two codes (tolerance mode; c = 0: MUFU, 1: poly).
+__device__ __forceinline__ uint32_t quad_codes2(float2 u, float sq, float cr, bool poly) {
+    const float2 t = ffma2(u, f2(sq), f2(cr));
+    const float2 y = poly ? exp2_poly2(t) : make_float2(ex2_approx(t.x), ex2_approx(t.y));
+    const float2 r = fadd2(y, f2(kMagic));
+    return __byte_perm(__float_as_uint(r.x), __float_as_uint(r.y), 0x0040) & 0xffffu;
+}
+
+template <int D>
+__device__ __forceinline__ void softmax_quad(Smem<D>& sm, const Params& p, uint32_t tmem,
+                                             uint32_t warp, uint32_t lane, uint32_t b_s_full,
+                                             uint32_t b_s_empty, uint32_t b_k_full,
+                                             uint32_t b_kv_empty, uint32_t b_p_full,
+                                             uint32_t b_p_empty, uint32_t b_pv_full,
+                                             uint32_t b_pv_empty) {
+    const float kNegInf = -__int_as_float(0x7f800000);
+    const bool causal = (p.flags & IFA_FLAG_CAUSAL) != 0;
+    const int32_t n = p.n;
+    const uint32_t quarter = warp & 3;
+    const uint32_t half = (warp - SOFT_WARP0) >> 2;   // which 16 rows of the quarter
+    const uint32_t t0 = lane & 3;                      // column pair within an 8-column group
+    const uint32_t lane_base = quarter * 32 + half * 16;
+    const int32_t row0 = static_cast<int32_t>(lane_base + (lane >> 2));  // and row0 + 8
+    const uint32_t t_base = tmem + (lane_base << 16);
+    Ring<STAGES> kv;
+    uint32_t i = 0, pi = 0, bi = 0;
+
+    for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x) {
+        const Work w = work_of(idx, p, causal);
+        int32_t grow[2];
+        float sq[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            grow[r] = w.q0 + row0 + 8 * r;
+            sq[r] = grow[r] < n ? p.sq[static_cast<int64_t>(w.slice) * n + grow[r]] : 0.0f;
+        }
+        float acc[2][D / 4];  // [row][column pair k*2 + e over this thread's D/4 columns]
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int c = 0; c < D / 4; ++c) acc[r][c] = 0.0f;
+        float l[2] = {0.0f, 0.0f}, m[2] = {kNegInf, kNegInf}, alpha[2] = {1.0f, 1.0f};
+        bool pend = false;
+
+        for (int32_t key0 = 0; key0 < w.kv_limit; key0 += BN) {
+            const uint32_t st = kv.idx;
+            bar_wait(b_s_full, i & 1);
+            tc_fence_after();
+            uint32_t sr[64];
+            {
+                uint32_t (&a)[16] = *reinterpret_cast<uint32_t(*)[16]>(&sr[0]);
+                uint32_t (&b)[16] = *reinterpret_cast<uint32_t(*)[16]>(&sr[16]);
+                uint32_t (&c)[16] = *reinterpret_cast<uint32_t(*)[16]>(&sr[32]);
+                uint32_t (&d)[16] = *reinterpret_cast<uint32_t(*)[16]>(&sr[48]);
+                tmem_ld_16x256b<16>(t_base + T_S + 0, a);
+                tmem_ld_16x256b<16>(t_base + T_S + 32, b);
+                tmem_ld_16x256b<16>(t_base + T_S + 64, c);
+                tmem_ld_16x256b<16>(t_base + T_S + 96, d);
+            }
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(b_s_empty);
+            bar_wait(b_k_full + 8 * st, kv.phase);
+            // u = float(S) * (sK * log2e [* extra]); sr[4k + {0,1}] row0, [4k + {2,3}] row1,
+            // columns 8k + 2*t0 + {0,1}
+            float u[64];
+            const float* skc = sm.sk[st] + 2 * t0;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const float2 s2 = *reinterpret_cast<const float2*>(skc + 8 * k);
+                const float2 a = fmul2(make_float2(__int2float_rn(static_cast<int32_t>(sr[4 * k])),
+                                                   __int2float_rn(static_cast<int32_t>(sr[4 * k + 1]))),
+                                       s2);
+                const float2 b = fmul2(make_float2(__int2float_rn(static_cast<int32_t>(sr[4 * k + 2])),
+                                                   __int2float_rn(static_cast<int32_t>(sr[4 * k + 3]))),
+                                       s2);
+                u[4 * k] = a.x;
+                u[4 * k + 1] = a.y;
+                u[4 * k + 2] = b.x;
+                u[4 * k + 3] = b.y;
+            }
+            __syncwarp();
+            if (lane == 0) bar_arrive(b_kv_empty + 8 * st);
+            // causal / ragged tail: keys >= the visible limit of each row
+            const int32_t tail = n - key0 < BN ? n - key0 : BN;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                int32_t lim = tail;
+                if (causal) {
+                    const int32_t vis = grow[r] - key0 + 1;
+                    if (vis < lim) lim = vis < 0 ? 0 : vis;
+                }
+                if (lim < BN) {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e)
+                            if (8 * k + 2 * static_cast<int32_t>(t0) + e >= lim)
+                                u[4 * k + 2 * r + e] = kNegInf;
+                }
+            }
+            // row maxima: 32 values per thread per row, then the quad
+            float mx[2];
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                float a[11];
+#pragma unroll
+                for (int j = 0; j < 10; ++j) {
+                    const int v0 = 3 * j, v1 = 3 * j + 1, v2 = 3 * j + 2;  // value index 2k + e
+                    a[j] = fmax3(u[4 * (v0 >> 1) + 2 * r + (v0 & 1)], u[4 * (v1 >> 1) + 2 * r + (v1 & 1)],
+                                 u[4 * (v2 >> 1) + 2 * r + (v2 & 1)]);
+                }
+                a[10] = fmaxf(u[4 * 15 + 2 * r], u[4 * 15 + 2 * r + 1]);
+                float b = fmaxf(fmax3(fmax3(a[0], a[1], a[2]), fmax3(a[3], a[4], a[5]),
+                                      fmax3(a[6], a[7], a[8])),
+                                fmaxf(a[9], a[10]));
+                b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, 1));
+                b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, 2));
+                mx[r] = b;
+            }
+            float mnew[2], cr[2];
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                mnew[r] = (m[r] < mx[r]) ? mx[r] : m[r];
+                cr[r] = kLog2_127 - sq[r] * mnew[r];
+            }
+            if (pi >= 2) {
+                bar_wait(b_p_empty + 8 * (pi & 1), ((pi - 2) >> 1) & 1);
+                tc_fence_after();
+            }
+            // codes -> P words: st.16x256b rep kp: {row0 word 2kp..., } = columns
+            // 8kp + 2t0 + {0,1}; word j0 = codes of k = 4kp + {0,1}, j0+1 = k = 4kp + {2,3}
+            uint32_t wd[16];
+#pragma unroll
+            for (int kp = 0; kp < 4; ++kp) {
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const int k = 4 * kp;
+                    const uint32_t c0 = quad_codes2(make_float2(u[4 * k + 2 * r], u[4 * k + 2 * r + 1]),
+                                                    sq[r], cr[r], false);
+                    const uint32_t c1 = quad_codes2(make_float2(u[4 * (k + 1) + 2 * r], u[4 * (k + 1) + 2 * r + 1]),
+                                                    sq[r], cr[r], false);
+                    const uint32_t c2 = quad_codes2(make_float2(u[4 * (k + 2) + 2 * r], u[4 * (k + 2) + 2 * r + 1]),
+                                                    sq[r], cr[r], false);
+                    const uint32_t c3 = quad_codes2(make_float2(u[4 * (k + 3) + 2 * r], u[4 * (k + 3) + 2 * r + 1]),
+                                                    sq[r], cr[r], true);
+                    wd[4 * kp + 2 * r] = c0 | (c1 << 16);
+                    wd[4 * kp + 2 * r + 1] = c2 | (c3 << 16);
+                }
+            }
+            tmem_st_16x256b_x4(t_base + T_P0 + 32 * (pi & 1), wd);
+            // fold the previous block's P.V: acc = acc*alpha + float(PV)
+            if (pend) {
+                bar_wait(b_pv_full, bi & 1);
+                tc_fence_after();
+                uint32_t rs[4];
+                tmem_ld_16x256b<4>(t_base + T_RS, rs);
+#pragma unroll
+                for (int ch = 0; ch < D / 32; ++ch) {
+                    uint32_t pv[16];
+                    tmem_ld_16x256b<16>(t_base + T_PV + 32 * ch, pv);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+#pragma unroll
+                        for (int r = 0; r < 2; ++r) {
+                            const int a = 8 * ch + 2 * k;  // pair index within acc[r]
+                            const float2 pf = make_float2(__int2float_rn(static_cast<int32_t>(pv[4 * k + 2 * r])),
+                                                          __int2float_rn(static_cast<int32_t>(pv[4 * k + 2 * r + 1])));
+                            const float2 o = ffma2(make_float2(acc[r][a], acc[r][a + 1]), f2(alpha[r]), pf);
+                            acc[r][a] = o.x;
+                            acc[r][a + 1] = o.y;
+                        }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) bar_arrive(b_pv_empty);
+                ++bi;
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+                    l[r] = __fmaf_rn(l[r], alpha[r],
+                                     static_cast<float>(static_cast<int32_t>(rs[2 * r])));
+                pend = false;
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(b_p_full + 8 * (pi & 1));
+            ++pi;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                alpha[r] = (mnew[r] == m[r]) ? 1.0f
+                           : (m[r] == kNegInf ? 0.0f : ex2_approx(sq[r] * (m[r] - mnew[r])));
+                m[r] = mnew[r];
+            }
+            pend = true;
+            kv.advance();
+            ++i;
+        }
+        // last block's fold, then O = acc * (sV / l)
+        bar_wait(b_pv_full, bi & 1);
+        tc_fence_after();
+        uint32_t rs[4];
+        tmem_ld_16x256b<4>(t_base + T_RS, rs);
+        const float sv = p.sv[w.slice];
+        float f[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            tmem_wait_ld();
+            l[r] = __fmaf_rn(l[r], alpha[r], static_cast<float>(static_cast<int32_t>(rs[2 * r])));
+            f[r] = __fdiv_rn(sv, l[r]);
+        }
+#pragma unroll
+        for (int ch = 0; ch < D / 32; ++ch) {
+            uint32_t pv[16];
+            tmem_ld_16x256b<16>(t_base + T_PV + 32 * ch, pv);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const int a = 8 * ch + 2 * k;
+                    const float2 pf = make_float2(__int2float_rn(static_cast<int32_t>(pv[4 * k + 2 * r])),
+                                                  __int2float_rn(static_cast<int32_t>(pv[4 * k + 2 * r + 1])));
+                    const float2 o = ffma2(make_float2(acc[r][a], acc[r][a + 1]), f2(alpha[r]), pf);
+                    acc[r][a] = o.x;
+                    acc[r][a + 1] = o.y;
+                }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) bar_arrive(b_pv_empty);
+        ++bi;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            if (grow[r] >= n) continue;
+            float* orow = p.o + (static_cast<int64_t>(w.slice) * n + grow[r]) * p.d;
+#pragma unroll
+            for (int k = 0; k < D / 8; ++k) {
+                const int col = 8 * k + 2 * static_cast<int>(t0);
+                if (col < p.d) {
+                    const float2 o = make_float2(acc[r][2 * k] * f[r], acc[r][2 * k + 1] * f[r]);
+                    if (col + 1 < p.d)
+                        __stcs(reinterpret_cast<float2*>(orow + col), o);
+                    else
+                        orow[col] = o.x;
+                }
+            }
+        }
+    }
+}
+
 // GENERIC = false: the benchmark-shaped fast path (non-causal, KV blocks
 // equal to the 128-key tiles, no audit, no 1/sqrt(d)); true: every feature,
 // selected at run time.
-template <int D, bool GENERIC, bool FAST>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+template <int D, bool GENERIC, bool FAST, bool QUAD>
+__global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_THREADS, 1)
     int_flash_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const Params p) {
+    // math warps: 16 (four per row, 32x32b) or 8 (quad layout, 16x256b)
+    constexpr int kMathWarps = QUAD ? QUAD_WARPS : SOFT_WARPS;
     constexpr uint32_t kLayout = D == 128 ? kLayoutSw128 : kLayoutSw64;
     constexpr uint32_t kSbo = 8 * D;  // 8 rows of D bytes per swizzle atom
     constexpr uint32_t kTileBytes = BN * D;
@@ -390,7 +688,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
-    const bool causal = GENERIC && (p.flags & IFA_FLAG_CAUSAL) != 0;
+    const bool causal = (GENERIC || QUAD) && (p.flags & IFA_FLAG_CAUSAL) != 0;
     const bool audit = GENERIC && p.audit != nullptr;
     const int32_t n = p.n;
 
@@ -407,18 +705,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int i = 0; i < 2; ++i) {
             mbar_init(&sm.q_full[i], 1);
             mbar_init(&sm.q_empty[i], 1);
-            mbar_init(&sm.p_full[i], SOFT_WARPS);
+            mbar_init(&sm.p_full[i], kMathWarps);
             mbar_init(&sm.p_empty[i], 1);
         }
         for (int i = 0; i < STAGES; ++i) {
             mbar_init(&sm.k_full[i], 32);
             mbar_init(&sm.v_full[i], 1);
-            mbar_init(&sm.kv_empty[i], 1 + SOFT_WARPS);
+            mbar_init(&sm.kv_empty[i], 1 + kMathWarps);
         }
         mbar_init(&sm.s_full, 1);
-        mbar_init(&sm.s_empty, SOFT_WARPS);
+        mbar_init(&sm.s_empty, kMathWarps);
         mbar_init(&sm.pv_full, 1);
-        mbar_init(&sm.pv_empty, SOFT_WARPS);
+        mbar_init(&sm.pv_empty, kMathWarps);
         fence_barrier_init();
     }
     if (threadIdx.x < 128) sm.bounds[threadIdx.x] = p.bounds[threadIdx.x];
@@ -433,7 +731,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tmem = sm.tmem_base;
 
     if (warp < SOFT_WARP0) {
-      regs_dealloc<kRegsControl>();
+      if constexpr (QUAD)
+          regs_dealloc<kRegsControlQuad>();
+      else
+          regs_dealloc<kRegsControl>();
       if (warp == 0) {
         // ------------------------------------------------------------ producer
         const uint64_t pol_stream = policy_evict_first();
@@ -481,8 +782,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     tma_load_3d(sm.k[st], &tm_k, &sm.k_full[st], 0, it.key0, w.slice, pol_keep);
                     if (it.kind & K_PV) {
                         mbar_arrive_expect_tx(&sm.v_full[st], kTileBytes);
-                        tma_load_3d(sm.v[st], &tm_v, &sm.v_full[st], 0, it.key0, w.slice,
-                                    pol_keep);
+                        if constexpr (QUAD)
+                            tma_load_5d(sm.v[st], &tm_v, &sm.v_full[st], 0, 0, 0, 0,
+                                        (w.slice * n + it.key0) / 32, pol_keep);
+                        else
+                            tma_load_3d(sm.v[st], &tm_v, &sm.v_full[st], 0, it.key0, w.slice,
+                                        pol_keep);
                     } else {
                         bar_arrive(b_v_full + 8 * st);
                     }
@@ -570,6 +875,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         __syncwarp();
       }
+    } else if constexpr (QUAD) {
+        regs_alloc<kRegsMathQuad>();
+        softmax_quad<D>(sm, p, tmem, warp, lane, b_s_full, b_s_empty, b_k_full, b_kv_empty,
+                        b_p_full, b_p_empty, b_pv_full, b_pv_empty);
     } else {
         regs_alloc<kRegsSoftmax>();
         // ------------------------------------------------- softmax + correction
@@ -929,13 +1238,37 @@ static bool make_map(CUtensorMap* map, const int8_t* base, int64_t slices, int64
     return r == CUDA_SUCCESS;
 }
 
-template <int D, bool GENERIC, bool FAST>
+// V as a 5-D view [k''][t0][m][e][d] with strides {32, 2, 8, 1} rows: one box
+// of 128 keys lands in shared memory with row p = e + 2m + 8t0 + 32k' holding
+// key e + 8m + 2t0 + 32k' (a 4x4 transpose of row pairs inside every 32-key
+// group), which is the key order of the quad kernel's packed P words.
+// Needs n % 32 == 0 (the slices are flattened into the k'' dimension).
+static bool make_map_vperm(CUtensorMap* map, const int8_t* base, int64_t slices, int64_t n,
+                           int64_t pitch, int D) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc || n % 32 != 0) return false;
+    const cuuint64_t dims[5] = {static_cast<cuuint64_t>(pitch), 2, 4, 4,
+                                static_cast<cuuint64_t>(slices * n / 32)};
+    const cuuint64_t strides[4] = {static_cast<cuuint64_t>(pitch),
+                                   static_cast<cuuint64_t>(8 * pitch),
+                                   static_cast<cuuint64_t>(2 * pitch),
+                                   static_cast<cuuint64_t>(32 * pitch)};
+    const cuuint32_t box[5] = {static_cast<cuuint32_t>(D), 2u, 4u, 4u, 4u};
+    const cuuint32_t estr[5] = {1u, 1u, 1u, 1u, 1u};
+    const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<int8_t*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           D == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int D, bool GENERIC, bool FAST, bool QUAD = false>
 static cudaError_t launch_k(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                             const Params& p, int64_t slices, cudaStream_t stream) {
     const size_t smem = sizeof(Smem<D>) + 1024;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(int_flash_fwd_kernel<D, GENERIC, FAST>,
+        cudaError_t e = cudaFuncSetAttribute(int_flash_fwd_kernel<D, GENERIC, FAST, QUAD>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
@@ -952,8 +1285,16 @@ static cudaError_t launch_k(const CUtensorMap& tq, const CUtensorMap& tk, const 
     }
     (void)slices;
     const int grid = p.items < sms ? p.items : sms;
-    int_flash_fwd_kernel<D, GENERIC, FAST><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+    constexpr int threads = QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_THREADS;
+    int_flash_fwd_kernel<D, GENERIC, FAST, QUAD><<<grid, threads, smem, stream>>>(tq, tk, tv, p);
     return cudaGetLastError();
+}
+
+// IFA_B200_NO_QUAD=1 selects the 16-warp tolerance kernel instead (A/B runs;
+// read at every call so a test can flip it).
+static bool quad_off() {
+    const char* e = getenv("IFA_B200_NO_QUAD");
+    return e && e[0] == '1';
 }
 
 template <int D>
@@ -986,7 +1327,13 @@ static cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
     const bool tiles_are_blocks = p.bc == BN || (p.bc == p.n && p.n <= BN);
     const bool generic = a.audit != nullptr || (a.flags & (IFA_FLAG_SQRT_D | IFA_FLAG_CAUSAL)) ||
                          !tiles_are_blocks;
-    // tolerance mode (no audit: the audit reports the exact codes)
+    // tolerance mode (no audit: the audit reports the exact codes); the quad
+    // kernel when the V view can be permuted
+    if ((a.flags & IFA_FLAG_FAST) && a.audit == nullptr && tiles_are_blocks && !quad_off()) {
+        CUtensorMap tvp;
+        if (make_map_vperm(&tvp, a.v, a.slices, a.n, a.pitch, D))
+            return launch_k<D, false, true, true>(tq, tk, tvp, p, a.slices, stream);
+    }
     if ((a.flags & IFA_FLAG_FAST) && a.audit == nullptr)
         return generic ? launch_k<D, true, true>(tq, tk, tv, p, a.slices, stream)
                        : launch_k<D, false, true>(tq, tk, tv, p, a.slices, stream);

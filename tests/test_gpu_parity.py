@@ -260,11 +260,13 @@ def _fast_close(got, want, vc, vs):
     return mre, float(np.abs(got.astype(np.float64) - want).max()), bound
 
 
-@pytest.mark.parametrize("n,d", [(1, 1), (24, 16), (128, 128), (300, 100), (1000, 128),
-                                 (4096, 128)])
+@pytest.mark.parametrize("n,d", [(1, 1), (24, 16), (96, 64), (128, 128), (224, 128),
+                                 (300, 100), (1000, 128), (1024, 64), (4096, 128)])
 @pytest.mark.parametrize("dist", ["normal", "uniform"])
 @pytest.mark.parametrize("causal", [False, True])
 def test_fast_mode_within_tolerance(ifa, oracle, n, d, dist, causal):
+    """n % 32 == 0 runs the quad-layout kernel (8 math warps); the others the
+    16-warp one."""
     _, (qc, qs, kc, ks, vc, vs) = _quantized_case(oracle, dist, n, d, seed=n + d)
     want = oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, 128,
                                       flags=2 if causal else 0)
@@ -289,3 +291,20 @@ def test_fast_mode_odd_blocks(ifa, oracle, n, d, bc):
         ifa.BlockSpec(64, bc), fast=True)).cpu().numpy()
     mre, mx, bound = _fast_close(got, want, vc, vs)
     assert mre <= FAST_MRE and mx <= bound, (mre, mx, bound)
+
+
+@pytest.mark.parametrize("n,d", [(256, 128), (2048, 64)])
+@pytest.mark.parametrize("causal", [False, True])
+def test_fast_mode_both_kernels_agree(ifa, oracle, n, d, causal, monkeypatch):
+    """The quad-layout (8 math warps) and 16-warp tolerance kernels compute
+    the same codes up to exp2-estimate ties: their outputs agree far inside
+    the tolerance.  IFA_B200_NO_QUAD=1 selects the 16-warp kernel."""
+    _, (qc, qs, kc, ks, vc, vs) = _quantized_case(oracle, "uniform", n, d, seed=n)
+    inputs = ifa.QuantizedAttentionInputs(
+        ifa.QuantizedRows(_dev(qc), _dev(qs)), ifa.QuantizedRows(_dev(kc), _dev(ks)),
+        ifa.QuantizedTensor(_dev(vc), _dev(np.asarray(vs, np.float32))))
+    cfg = ifa.AttentionConfig(ifa.BlockSpec(64, 128), causal=causal, fast=True)
+    a = ifa.int_flash_attention(inputs, cfg).cpu().numpy().astype(np.float64)
+    monkeypatch.setenv("IFA_B200_NO_QUAD", "1")
+    b = ifa.int_flash_attention(inputs, cfg).cpu().numpy().astype(np.float64)
+    assert np.abs(a - b).sum() / np.abs(b).sum() <= 1e-5
