@@ -10,12 +10,19 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 PKG := paper_2409_16997_b200
 CSRC := $(PKG)/csrc
 LIB := $(PKG)/lib/libifa_b200.so
-SRCS := $(CSRC)/abi.cu $(CSRC)/host_abi.cu $(CSRC)/attn.cu $(CSRC)/quant.cu $(CSRC)/code_bounds.cpp
+SRCS := $(CSRC)/abi.cu $(CSRC)/host_abi.cu $(CSRC)/attn.cu $(CSRC)/quant.cu $(CSRC)/code_bounds.cpp \
+        $(CSRC)/tensor_io.cpp
 HDRS := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/ifa_b200.h
 NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=false \
            -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 
-all: $(LIB) oracle
+CLI := $(PKG)/lib/ifa_b200
+
+all: $(LIB) $(CLI) oracle
+
+# command-line front end (quantize / info on IFA1 files), C++ over the C-ABI
+$(CLI): tools/ifa_b200_cli.cpp include/ifa_b200.h $(LIB)
+	g++ -O2 -std=c++17 -Iinclude -o $@ $< -L$(PKG)/lib -lifa_b200 -Wl,-rpath,'$$ORIGIN'
 
 $(LIB): $(SRCS) $(HDRS)
 	@mkdir -p $(PKG)/lib

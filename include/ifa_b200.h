@@ -46,6 +46,7 @@ extern "C" {
 #define IFA_EOVERFLOW 75  /* std::overflow_error (int32 depth guard)      */
 #define IFA_ENOTSUP 95    /* shape this build does not run on the GPU     */
 #define IFA_ECUDA 1000    /* CUDA runtime / driver error                  */
+#define IFA_EFORMAT 74    /* ifa::FormatError (malformed IFA1 tensor file) */
 
 /* ifa_int_flash_fwd flags */
 #define IFA_FLAG_SQRT_D 1u /* AttentionConfig::apply_sqrt_d_scaling (attention.hpp:25-27) */
@@ -130,6 +131,23 @@ int ifa_audit_init(ifa_pcode_audit* audit, void* stream);
  * (int)roundf(127*expf(x)) >= k+1 (k < 127), out128[127] = +inf.  Exposed so
  * tests can check them against an exhaustive scan of the reference's libm. */
 int ifa_code_bounds(float* out128);
+
+/* ---- IFA1 tensor files (tensor_io.hpp:22-39, tensor_io.cpp:15-178) ------
+ * "IFA1" | dtype u8 (IFA_DT_*) | 3 zero bytes | rows u64 LE | cols u64 LE |
+ * row-major payload.  Loaders reject malformed files with IFA_EFORMAT and
+ * the reference's FormatError message ("bad magic", "truncated header: N
+ * bytes", "nonzero reserved bytes", "header dimensions overflow: RxC",
+ * "bad dtype code D", "truncated payload: ...", "oversized payload: ...",
+ * "expected f32 tensor: PATH", "cannot open: PATH").  Host memory. */
+#define IFA_DT_F32 0
+#define IFA_DT_I8 1
+#define IFA_DT_I32 2
+int ifa_tensor_save(const char* path, int32_t dtype, const void* data, int64_t rows,
+                    int64_t cols);
+/* Validates the whole file (header and payload size) and reports its shape. */
+int ifa_tensor_info(const char* path, int32_t* dtype, int64_t* rows, int64_t* cols);
+/* dtype < 0 accepts any dtype; rows/cols must match the file (ifa_tensor_info). */
+int ifa_tensor_load(const char* path, int32_t dtype, void* data, int64_t rows, int64_t cols);
 
 /* Message of the last failing call on this host thread ("" if none). */
 const char* ifa_last_error(void);

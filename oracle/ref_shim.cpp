@@ -21,6 +21,7 @@
 #include "ifa/generate.hpp"
 #include "ifa/oracles.hpp"
 #include "ifa/quant.hpp"
+#include "ifa/tensor_io.hpp"
 #include "ifa/verify.hpp"
 
 namespace {
@@ -55,6 +56,50 @@ ifa::QuantizedAttentionInputs make_inputs(const int8_t* q, const float* sq, cons
 extern "C" {
 
 const char* ifa_ref_last_error() { return g_err.c_str(); }
+
+// IFA1 files through the reference's own tensor_io (format cross-checks).
+int ifa_ref_save_tensor(const char* path, int dtype, const void* data, int64_t rows,
+                        int64_t cols) {
+    try {
+        if (dtype == 0) {
+            const float* p = static_cast<const float*>(data);
+            ifa::save_tensor(ifa::FloatMatrix(rows, cols, std::vector<float>(p, p + rows * cols)),
+                             path);
+        } else if (dtype == 1) {
+            const int8_t* p = static_cast<const int8_t*>(data);
+            ifa::save_tensor(
+                ifa::Int8Matrix(rows, cols, std::vector<int8_t>(p, p + rows * cols)), path);
+        } else {
+            const int32_t* p = static_cast<const int32_t*>(data);
+            ifa::save_tensor(
+                ifa::Int32Matrix(rows, cols, std::vector<int32_t>(p, p + rows * cols)), path);
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// Loads with ifa::load_tensor; fills dtype/rows/cols and copies the payload
+// when it fits `capacity` bytes.  On FormatError returns -1 with the message.
+int ifa_ref_load_tensor(const char* path, int* dtype, int64_t* rows, int64_t* cols, void* buf,
+                        int64_t capacity) {
+    try {
+        const ifa::LoadedTensor t = ifa::load_tensor(path);
+        *dtype = static_cast<int>(ifa::loaded_dtype(t));
+        std::visit(
+            [&](const auto& m) {
+                *rows = m.rows();
+                *cols = m.cols();
+                const int64_t bytes = m.size() * static_cast<int64_t>(sizeof(m.data()[0]));
+                if (buf && bytes <= capacity) std::memcpy(buf, m.data(), static_cast<size_t>(bytes));
+            },
+            t);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
 
 int ifa_ref_generate(int dist, double a, double b, uint64_t seed, int64_t rows, int64_t cols,
                      float* out) {

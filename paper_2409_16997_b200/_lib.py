@@ -16,6 +16,7 @@ IFA_EINVAL = 22
 IFA_EOVERFLOW = 75
 IFA_ENOTSUP = 95
 IFA_ECUDA = 1000
+IFA_EFORMAT = 74
 
 FLAG_SQRT_D = 1
 FLAG_CAUSAL = 2
@@ -29,6 +30,9 @@ EXPORTED_SYMBOLS = (
     "ifa_quantize_per_row_host",
     "ifa_quantize_per_tensor_host",
     "ifa_int_flash_fwd_host",
+    "ifa_tensor_save",
+    "ifa_tensor_info",
+    "ifa_tensor_load",
     "ifa_audit_init",
     "ifa_code_bounds",
     "ifa_last_error",
@@ -38,6 +42,10 @@ EXPORTED_SYMBOLS = (
 
 class NativeLibraryError(RuntimeError):
     pass
+
+
+class FormatError(RuntimeError):
+    """Malformed IFA1 tensor file (ifa::FormatError, tensor_io.hpp:16-20)."""
 
 
 class PCodeAuditC(C.Structure):
@@ -79,6 +87,13 @@ def load() -> C.CDLL:
     lib.ifa_int_flash_fwd_host.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64,
                                            u32, vp, vp]
     lib.ifa_int_flash_fwd_host.restype = C.c_int
+    i32 = C.c_int32
+    lib.ifa_tensor_save.argtypes = [C.c_char_p, i32, vp, i64, i64]
+    lib.ifa_tensor_save.restype = C.c_int
+    lib.ifa_tensor_info.argtypes = [C.c_char_p, C.POINTER(i32), C.POINTER(i64), C.POINTER(i64)]
+    lib.ifa_tensor_info.restype = C.c_int
+    lib.ifa_tensor_load.argtypes = [C.c_char_p, i32, vp, i64, i64]
+    lib.ifa_tensor_load.restype = C.c_int
     lib.ifa_audit_init.argtypes = [vp, vp]
     lib.ifa_audit_init.restype = C.c_int
     lib.ifa_code_bounds.argtypes = [vp]
@@ -100,6 +115,8 @@ def check(rc: int) -> None:
         raise ValueError(msg)          # std::invalid_argument
     if rc == IFA_EOVERFLOW:
         raise OverflowError(msg)       # std::overflow_error
+    if rc == IFA_EFORMAT:
+        raise FormatError(msg)         # ifa::FormatError
     if rc == IFA_ENOTSUP:
         raise NotImplementedError(msg)
     raise NativeLibraryError(f"CUDA failure ({rc}): {msg}")
