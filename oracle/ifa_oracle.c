@@ -424,6 +424,89 @@ int ifa_or_int_flash_attention_batched(const int8_t *q, const float *sq, const i
 /* ------------------------------------------------------------------ */
 /* oracles.cpp:83-134 untiled integer attention (+ causal)              */
 /* ------------------------------------------------------------------ */
+/* half-INT8 attention (attention.cpp:359-399): integer scores scaled by
+ * the per-row Q/K scales, then the float tiled flash path
+ * (tiled_float_attention :49-80, merge_softmax_state :91-137,
+ * finalize_softmax_state :139-149) on float V.  Every float expression in
+ * the reference's order; -ffp-contract=off (no FMA), like the reference's
+ * build.  No causal mode (the reference has none; this build's GPU
+ * half-INT8 kernel refuses it too). */
+int ifa_or_half_int8_attention(const int8_t *q, const float *sq, const int8_t *k,
+                               const float *sk, const float *v, int64_t n, int64_t d,
+                               int64_t br_cfg, int64_t bc_cfg, uint32_t flags, float *out) {
+    if (n < 1 || d < 1) return -1;                       /* :372-374 */
+    if (br_cfg < 1 || bc_cfg < 1) return -1;             /* cfg.validate() */
+    if (d > IFA_MAX_INT_GEMM_DEPTH) return -2;           /* :375 */
+    const float extra = (flags & IFA_OR_FLAG_SQRT_D) ? 1.0f / sqrtf((float)d) : 1.0f;
+    const int64_t br_max = br_cfg < n ? br_cfg : n;
+    const int64_t bc_max = bc_cfg < n ? bc_cfg : n;
+    float *s = (float *)malloc(sizeof(float) * br_max * bc_max);
+    float *p = (float *)malloc(sizeof(float) * br_max * bc_max);
+    float *acc = (float *)malloc(sizeof(float) * br_max * d);
+    float *m = (float *)malloc(sizeof(float) * br_max);
+    float *l = (float *)malloc(sizeof(float) * br_max);
+    if (!s || !p || !acc || !m || !l) return -3;
+    for (int64_t i0 = 0; i0 < n; i0 += br_cfg) {
+        const int64_t br = (br_cfg < n - i0) ? br_cfg : n - i0;
+        for (int64_t r = 0; r < br; ++r) {
+            m[r] = -INFINITY;
+            l[r] = 0.0f;
+        }
+        memset(acc, 0, sizeof(float) * br * d);
+        for (int64_t j0 = 0; j0 < n; j0 += bc_cfg) {
+            const int64_t bc = (bc_cfg < n - j0) ? bc_cfg : n - j0;
+            /* fill (:378-394): s = float(S_int) * (sq * sk) [*= extra] */
+            for (int64_t r = 0; r < br; ++r) {
+                const float sqr = sq[i0 + r];
+                for (int64_t c = 0; c < bc; ++c) {
+                    int32_t a = 0;
+                    const int8_t *qr = q + (i0 + r) * d;
+                    const int8_t *kc = k + (j0 + c) * d;
+                    for (int64_t t = 0; t < d; ++t) a += (int32_t)qr[t] * (int32_t)kc[t];
+                    s[r * bc + c] = (float)a * (sqr * sk[j0 + c]);
+                }
+                if (extra != 1.0f)
+                    for (int64_t c = 0; c < bc; ++c) s[r * bc + c] *= extra;
+            }
+            /* merge_softmax_state (:114-136) */
+            for (int64_t r = 0; r < br; ++r) {
+                float m_loc = -INFINITY;
+                for (int64_t c = 0; c < bc; ++c)
+                    m_loc = (m_loc < s[r * bc + c]) ? s[r * bc + c] : m_loc;
+                const float m_new = (m[r] < m_loc) ? m_loc : m[r];
+                const float alpha = ifa_or_expf(m[r] - m_new);
+                float row_sum = 0.0f;
+                for (int64_t c = 0; c < bc; ++c) {
+                    const float e = ifa_or_expf(s[r * bc + c] - m_new);
+                    p[r * bc + c] = e;
+                    row_sum += e;
+                }
+                l[r] = l[r] * alpha + row_sum;
+                for (int64_t c = 0; c < d; ++c) acc[r * d + c] *= alpha;
+                m[r] = m_new;
+            }
+            /* float_gemm_nn_acc_strided (gemm.cpp:80-95) */
+            for (int64_t r = 0; r < br; ++r)
+                for (int64_t t = 0; t < bc; ++t) {
+                    const float av = p[r * bc + t];
+                    const float *bt = v + (j0 + t) * d;
+                    for (int64_t c = 0; c < d; ++c) acc[r * d + c] += av * bt[c];
+                }
+        }
+        /* finalize_softmax_state (:139-149) */
+        for (int64_t r = 0; r < br; ++r) {
+            const float inv = 1.0f / l[r];
+            for (int64_t c = 0; c < d; ++c) out[(i0 + r) * d + c] = acc[r * d + c] * inv;
+        }
+    }
+    free(s);
+    free(p);
+    free(acc);
+    free(m);
+    free(l);
+    return 0;
+}
+
 int ifa_or_untiled_int8_attention(const int8_t *q, const float *sq, const int8_t *k,
                                   const float *sk, const int8_t *v, float sv, int64_t n,
                                   int64_t d, uint32_t flags, float *out) {

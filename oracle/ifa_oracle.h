@@ -78,6 +78,9 @@ int ifa_or_untiled_int8_attention(const int8_t *q, const float *sq, const int8_t
                                   int64_t d, uint32_t flags, float *out);
 
 /* attention.cpp:151-192 fp64 ground truth (plus causal extension). */
+int ifa_or_half_int8_attention(const int8_t *q, const float *sq, const int8_t *k,
+                               const float *sk, const float *v, int64_t n, int64_t d,
+                               int64_t br, int64_t bc, uint32_t flags, float *out);
 int ifa_or_reference_attention(const float *q, const float *k, const float *v, int64_t n,
                                int64_t m, int64_t d, int64_t dv, uint32_t flags, float *out);
 

@@ -227,6 +227,23 @@ int ifa_ref_reference_attention(const float* q, const float* k, const float* v, 
     }
 }
 
+int ifa_ref_half_int8_attention(const int8_t* q, const float* sq, const int8_t* k,
+                                const float* sk, const float* v, int64_t n, int64_t d,
+                                int64_t br, int64_t bc, int sqrt_d, float* out) {
+    try {
+        ifa::QuantizedRows qr{to_im(q, n, d), ifa::ScaleVector(std::vector<float>(sq, sq + n))};
+        ifa::QuantizedRows kr{to_im(k, n, d), ifa::ScaleVector(std::vector<float>(sk, sk + n))};
+        ifa::AttentionConfig cfg;
+        cfg.blocks = ifa::BlockSpec{br, bc};
+        cfg.apply_sqrt_d_scaling = sqrt_d != 0;
+        const ifa::FloatMatrix o = ifa::half_int8_attention(qr, kr, to_fm(v, n, d), cfg);
+        std::memcpy(out, o.data(), sizeof(float) * static_cast<size_t>(n * d));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 float ifa_ref_expf(float x) { return std::exp(x); }
 
 }  // extern "C"

@@ -76,6 +76,9 @@ class Oracle:
             _i8p, _f32p, _i8p, _f32p, _i8p, C.c_float, C.c_int64, C.c_int64, C.c_uint32, _f32p]
         L.ifa_or_reference_attention.argtypes = [_f32p, _f32p, _f32p, C.c_int64, C.c_int64,
                                                  C.c_int64, C.c_int64, C.c_uint32, _f32p]
+        L.ifa_or_half_int8_attention.argtypes = [_i8p, _f32p, _i8p, _f32p, _f32p, C.c_int64,
+                                                 C.c_int64, C.c_int64, C.c_int64, C.c_uint32,
+                                                 _f32p]
         L.ifa_or_error_accum.argtypes = [_f32p, _f32p, C.c_int64, C.POINTER(C.c_double),
                                          C.POINTER(C.c_double)]
         L.ifa_or_fnv1a64.restype = C.c_uint64
@@ -166,6 +169,16 @@ class Oracle:
             raise ValueError("untiled: invalid argument")
         return out
 
+    def half_int8_attention(self, q, sq, k, sk, v, br=64, bc=64, flags=0):
+        q, k = _i8(q), _i8(k)
+        n, d = q.shape
+        out = np.empty((n, d), np.float32)
+        rc = self.lib.ifa_or_half_int8_attention(q, _f32(sq), k, _f32(sk), _f32(v), n, d, br,
+                                                 bc, flags, out)
+        if rc:
+            raise ValueError("half_int8_attention: invalid argument")
+        return out
+
     def reference_attention(self, q, k, v, flags=0):
         q, k, v = _f32(q), _f32(k), _f32(v)
         out = np.empty((q.shape[0], v.shape[1]), np.float32)
@@ -213,6 +226,9 @@ class Reference:
         L.ifa_ref_untiled_int8_attention.argtypes = [
             _i8p, _f32p, _i8p, _f32p, _i8p, C.c_float, C.c_int64, C.c_int64, C.c_int, _f32p]
         L.ifa_ref_reference_attention.argtypes = [_f32p, _f32p, _f32p, C.c_int64, C.c_int64,
+                                                  _f32p]
+        L.ifa_ref_half_int8_attention.argtypes = [_i8p, _f32p, _i8p, _f32p, _f32p, C.c_int64,
+                                                  C.c_int64, C.c_int64, C.c_int64, C.c_int,
                                                   _f32p]
         L.ifa_ref_expf.restype = C.c_float
         L.ifa_ref_expf.argtypes = [C.c_float]
@@ -293,3 +309,11 @@ class Reference:
 
     def expf(self, x):
         return self.lib.ifa_ref_expf(float(x))
+
+    def half_int8_attention(self, q, sq, k, sk, v, br=64, bc=64, sqrt_d=False):
+        q, k = _i8(q), _i8(k)
+        n, d = q.shape
+        out = np.empty((n, d), np.float32)
+        self._check(self.lib.ifa_ref_half_int8_attention(q, _f32(sq), k, _f32(sk), _f32(v), n, d,
+                                                         br, bc, int(sqrt_d), out))
+        return out
