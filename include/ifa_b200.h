@@ -103,6 +103,24 @@ int ifa_int_flash_fwd(const int8_t* q, const float* sq, const int8_t* k, const f
                       int64_t d, int64_t br, int64_t bc, uint32_t flags,
                       ifa_pcode_audit* audit, void* stream);
 
+/* ---- half-INT8 attention ----------------------------
+ * ifa_half_int8_fwd  replaces ifa::half_int8_attention (attention.hpp:93-96,
+ *                    attention.cpp:359-399): int8 Q/K with per-row scales
+ *                    (S exact int32 as above), float V and float weights.
+ * v_f16: DEVICE [slices][n][d] IEEE fp16 copy of V (ifa_convert_f16); the
+ * weights are fed to the tensor core as fp16 and accumulated in fp32.
+ * Tolerance semantics (tests/test_gpu_half.py): MRE against the reference
+ * <= 2e-3, and the error against fp64 within 1% of the reference's own.
+ * br/bc are validated as in the reference but only change float rounding
+ * order there, so the kernel tiles 128 x 128 regardless.  flags: SQRT_D
+ * only (the reference has no causal half-INT8 path).  Supported: d in {64,
+ * 128}; others return IFA_ENOTSUP. */
+int ifa_half_int8_fwd(const int8_t* q, const float* sq, const int8_t* k, const float* sk,
+                      const uint16_t* v_f16, float* o, int64_t slices, int64_t n, int64_t d,
+                      int64_t br, int64_t bc, uint32_t flags, void* stream);
+/* DEVICE x[count] f32 -> out[count] fp16 (round to nearest even). */
+int ifa_convert_f16(const float* x, int64_t count, uint16_t* out, void* stream);
+
 /* ---- host-buffer forms (drop-in for synchronous CPU callers) -------------
  * Same arguments as above, but every array is HOST memory (pageable or
  * pinned) and the call returns after the results are back on the host.

@@ -12,6 +12,7 @@ from .api import (  # noqa: F401
     QuantizedAttentionInputs,
     QuantizedRows,
     QuantizedTensor,
+    half_int8_attention,
     int_flash_attention,
     quantize_per_row,
     quantize_per_tensor,
@@ -21,6 +22,6 @@ from ._lib import NativeLibraryError  # noqa: F401
 
 __all__ = [
     "AttentionConfig", "BlockSpec", "PCodeAudit", "QuantizedAttentionInputs",
-    "QuantizedRows", "QuantizedTensor", "int_flash_attention", "quantize_per_row",
+    "QuantizedRows", "QuantizedTensor", "half_int8_attention", "int_flash_attention", "quantize_per_row",
     "quantize_per_tensor", "version", "NativeLibraryError",
 ]

@@ -17,6 +17,7 @@ reference                      here
                                (attention.hpp:63-70, attention.cpp:213-233)
 ``PCodeAudit``                 :class:`PCodeAudit` (attention.hpp:75-80)
 ``int_flash_attention``        :func:`int_flash_attention` (attention.hpp:85-87)
+``half_int8_attention``        :func:`half_int8_attention` (attention.hpp:93-96)
 =============================  ==============================================
 
 Tensors are ``torch`` CUDA tensors (PyTorch is only the device-memory and
@@ -234,6 +235,57 @@ def int_flash_attention(inputs: QuantizedAttentionInputs,
         audit.max_code = int(w[1])
         audit.row_max_block_hits_127 = bool(w[2])
         audit.rows_audited = int(raw[2])
+    return out
+
+
+def half_int8_attention(q: QuantizedRows, k: QuantizedRows, v: torch.Tensor,
+                        cfg: Optional[AttentionConfig] = None, *,
+                        out: Optional[torch.Tensor] = None,
+                        stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """Half-INT8 attention (attention.hpp:93-96, attention.cpp:359-399) on the GPU.
+
+    int8 Q/K with per-row scales, float V and float attention weights.  V
+    (f32 ``[..., n, d]``) is converted to fp16 on the device and the weights
+    go to the tensor core as fp16 with fp32 accumulation: O agrees with the
+    reference within the tolerance tests/test_gpu_half.py states, not
+    bitwise.  ``cfg.blocks`` is validated (it changes only float rounding
+    order in the reference); ``causal``/``fast`` are not part of this path.
+    """
+    cfg = cfg or AttentionConfig()
+    qv, kv = q.values, k.values
+    _require_cuda(qv, torch.int8, "half_int8_attention: q")
+    _require_cuda(kv, torch.int8, "half_int8_attention: k")
+    _require_cuda(v, torch.float32, "half_int8_attention: v")
+    if qv.dim() < 2 or qv.shape[-2] < 1 or qv.shape[-1] < 1 or v.shape[-1] < 1:
+        raise ValueError("half_int8_attention: empty input")       # attention.cpp:374-376
+    if kv.shape[-1] != qv.shape[-1]:
+        raise ValueError("half_int8_attention: q/k head dims differ")  # :364-366
+    if kv.shape[-2] != v.shape[-2]:
+        raise ValueError("half_int8_attention: k/v row counts differ")  # :367-369
+    if tuple(q.scales.shape) != tuple(qv.shape[:-1]) or \
+            tuple(k.scales.shape) != tuple(kv.shape[:-1]):
+        raise ValueError("half_int8_attention: scale length mismatch")  # :370-373
+    if tuple(kv.shape) != tuple(qv.shape) or tuple(v.shape) != tuple(qv.shape):
+        raise NotImplementedError(
+            "half_int8_attention: the sm_100a kernel takes q, k, v of one shape [..., n, d]")
+    cfg.validate()
+    if cfg.causal or cfg.fast:
+        raise NotImplementedError("half_int8_attention: causal/fast are not part of this path")
+    n, d = qv.shape[-2], qv.shape[-1]
+    slices = qv.numel() // (n * d)
+    qc, kc = qv.contiguous(), kv.contiguous()
+    sq, sk = q.scales.contiguous(), k.scales.contiguous()
+    vc = v.contiguous()
+    vh = torch.empty(v.shape, dtype=torch.float16, device=v.device)
+    if out is None:
+        out = torch.empty(qv.shape, dtype=torch.float32, device=qv.device)
+    lib = _lib.load()
+    sp = _stream_ptr(stream)
+    _lib.check(lib.ifa_convert_f16(vc.data_ptr(), vc.numel(), vh.data_ptr(), sp))
+    _lib.check(lib.ifa_half_int8_fwd(qc.data_ptr(), sq.data_ptr(), kc.data_ptr(), sk.data_ptr(),
+                                     vh.data_ptr(), out.data_ptr(), slices, n, d,
+                                     cfg.blocks.Br, cfg.blocks.Bc,
+                                     _lib.FLAG_SQRT_D if cfg.apply_sqrt_d_scaling else 0, sp))
     return out
 
 

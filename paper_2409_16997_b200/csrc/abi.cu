@@ -179,4 +179,47 @@ int ifa_int_flash_fwd(const int8_t* q, const float* sq, const int8_t* k, const f
     return e == cudaSuccess ? IFA_OK : cuda_fail(e, "int_flash_attention");
 }
 
+int ifa_half_int8_fwd(const int8_t* q, const float* sq, const int8_t* k, const float* sk,
+                      const uint16_t* v_f16, float* o, int64_t slices, int64_t n, int64_t d,
+                      int64_t br, int64_t bc, uint32_t flags, void* stream) {
+    g_err.clear();
+    if (slices < 0) return fail(IFA_EINVAL, "half_int8_attention: negative slice count");
+    // attention.cpp:374-376, gemm.cpp:16-20 (tiled_float_attention's cfg.validate)
+    if (n < 1 || d < 1) return fail(IFA_EINVAL, "half_int8_attention: empty input");
+    if (d > IFA_MAX_INT_GEMM_DEPTH)
+        return fail(IFA_EOVERFLOW, "int gemm depth " + std::to_string(d) +
+                                       " exceeds 133144; int32 accumulation could overflow");
+    if (br < 1 || bc < 1) return fail(IFA_EINVAL, "BlockSpec: Br and Bc must be >= 1");
+    if (flags & ~IFA_FLAG_SQRT_D) {
+        if (flags & ~(IFA_FLAG_SQRT_D | IFA_FLAG_CAUSAL | IFA_FLAG_FAST))
+            return fail(IFA_EINVAL, "half_int8_attention: unknown flag bits");
+        return fail(IFA_ENOTSUP, "half_int8_attention: only IFA_FLAG_SQRT_D is supported");
+    }
+    if (d != 64 && d != 128)
+        return fail(IFA_ENOTSUP, "half_int8_attention: head dim " + std::to_string(d) +
+                                     " not supported by the sm_100a kernel (64 or 128)");
+    if (slices == 0) return IFA_OK;
+    if (((n + 127) / 128) * slices > INT32_MAX)
+        return fail(IFA_ENOTSUP, "half_int8_attention: more than 2^31 (q tile, slice) work items");
+    if (!q || !sq || !k || !sk || !v_f16 || !o)
+        return fail(IFA_EINVAL, "half_int8_attention: null pointer");
+    if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) |
+         reinterpret_cast<uintptr_t>(v_f16)) % 16 != 0)
+        return fail(IFA_EINVAL, "half_int8_attention: q/k/v must be 16-byte aligned");
+    const cudaError_t e = ifa_b200::launch_half_int8_fwd(
+        q, sq, k, sk, v_f16, o, slices, n, d, d, (flags & IFA_FLAG_SQRT_D) != 0,
+        static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? IFA_OK : cuda_fail(e, "half_int8_attention");
+}
+
+int ifa_convert_f16(const float* x, int64_t count, uint16_t* out, void* stream) {
+    g_err.clear();
+    if (count < 0) return fail(IFA_EINVAL, "convert_f16: negative count");
+    if (count == 0) return IFA_OK;
+    if (!x || !out) return fail(IFA_EINVAL, "convert_f16: null pointer");
+    const cudaError_t e =
+        ifa_b200::launch_convert_f16(x, count, out, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? IFA_OK : cuda_fail(e, "convert_f16");
+}
+
 }  // extern "C"

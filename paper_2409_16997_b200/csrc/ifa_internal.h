@@ -44,4 +44,12 @@ struct AttnArgs {
 // makes zero-padded copies when d % 16 != 0); columns >= d must be zero.
 cudaError_t launch_int_flash_fwd(const AttnArgs& a, cudaStream_t stream);
 
+// attn_half.cu: half-INT8 forward (q/k codes of row pitch `pitch`, v fp16
+// [slices][n][d] dense, d in {64, 128}) and the f32 -> fp16 conversion.
+cudaError_t launch_half_int8_fwd(const int8_t* q, const float* sq, const int8_t* k,
+                                 const float* sk, const uint16_t* v, float* o, int64_t slices,
+                                 int64_t n, int64_t d, int64_t pitch, bool sqrt_d,
+                                 cudaStream_t stream);
+cudaError_t launch_convert_f16(const float* x, int64_t count, uint16_t* out, cudaStream_t stream);
+
 }  // namespace ifa_b200
