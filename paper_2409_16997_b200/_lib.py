@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libifa_b200.so")
+# IFA_B200_LIB: load an alternative build (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("IFA_B200_LIB") or os.path.join(_HERE, "lib", "libifa_b200.so")
 
 IFA_OK = 0
 IFA_EINVAL = 22

@@ -412,12 +412,21 @@ __device__ __forceinline__ void tmem_st_16x256b_x4(uint32_t taddr, const uint32_
         : "memory");
 }
 
-// Two values of one row -> two codes (tolerance mode; c = 0: MUFU, 1: poly).
-__device__ __forceinline__ uint32_t quad_codes2(float2 u, float sq, float cr, bool poly) {
+#ifndef IFA_QUAD_POLY
+#define IFA_QUAD_POLY 1  // exp2 pairs per 4 evaluated on the FMA pipe
+#endif
+
+// Rounds a pair of exp2 estimates to codes: the magic add leaves the integer
+// in the low byte of each float's bits.
+__device__ __forceinline__ float2 quad_round2(float2 u, float sq, float cr, bool poly) {
     const float2 t = ffma2(u, f2(sq), f2(cr));
     const float2 y = poly ? exp2_poly2(t) : make_float2(ex2_approx(t.x), ex2_approx(t.y));
-    const float2 r = fadd2(y, f2(kMagic));
-    return __byte_perm(__float_as_uint(r.x), __float_as_uint(r.y), 0x0040) & 0xffffu;
+    return fadd2(y, f2(kMagic));
+}
+// Low bytes of (a.x, a.y, b.x, b.y) -> one packed P word (three PRMTs).
+__device__ __forceinline__ uint32_t pack4(float2 a, float2 b) {
+    return __byte_perm(__byte_perm(__float_as_uint(a.x), __float_as_uint(a.y), 0x0040),
+                       __byte_perm(__float_as_uint(b.x), __float_as_uint(b.y), 0x0040), 0x5410);
 }
 
 template <int D>
@@ -455,6 +464,42 @@ __device__ __forceinline__ void softmax_quad(Smem<D>& sm, const Params& p, uint3
             for (int c = 0; c < D / 4; ++c) acc[r][c] = 0.0f;
         float l[2] = {0.0f, 0.0f}, m[2] = {kNegInf, kNegInf}, alpha[2] = {1.0f, 1.0f};
         bool pend = false;
+
+        // acc = acc*alpha + float(PV), l = l*alpha + rowsum for the finished
+        // block; all TMEM loads in flight before one wait.
+        auto fold = [&]() {
+            bar_wait(b_pv_full, bi & 1);
+            tc_fence_after();
+            uint32_t rs[4];
+            uint32_t pv[D / 2];
+            tmem_ld_16x256b<4>(t_base + T_RS, rs);
+#pragma unroll
+            for (int ch = 0; ch < D / 32; ++ch)
+                tmem_ld_16x256b<16>(t_base + T_PV + 32 * ch,
+                                    *reinterpret_cast<uint32_t(*)[16]>(&pv[16 * ch]));
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(b_pv_empty);
+            ++bi;
+#pragma unroll
+            for (int ch = 0; ch < D / 32; ++ch)
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        const int a = 8 * ch + 2 * k;  // pair index within acc[r]
+                        const uint32_t* q = &pv[16 * ch + 4 * k + 2 * r];
+                        const float2 pf = make_float2(__int2float_rn(static_cast<int32_t>(q[0])),
+                                                      __int2float_rn(static_cast<int32_t>(q[1])));
+                        const float2 o = ffma2(make_float2(acc[r][a], acc[r][a + 1]), f2(alpha[r]), pf);
+                        acc[r][a] = o.x;
+                        acc[r][a + 1] = o.y;
+                    }
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+                l[r] = __fmaf_rn(l[r], alpha[r], static_cast<float>(static_cast<int32_t>(rs[2 * r])));
+        };
 
         for (int32_t key0 = 0; key0 < w.kv_limit; key0 += BN) {
             const uint32_t st = kv.idx;
@@ -544,57 +589,29 @@ __device__ __forceinline__ void softmax_quad(Smem<D>& sm, const Params& p, uint3
                 tc_fence_after();
             }
             // codes -> P words: st.16x256b rep kp: {row0 word 2kp..., } = columns
-            // 8kp + 2t0 + {0,1}; word j0 = codes of k = 4kp + {0,1}, j0+1 = k = 4kp + {2,3}
+            // 8kp + 2t0 + {0,1}; word j0 = codes of k = 4kp + {0,1}, j0+1 = k = 4kp + {2,3}.
+            // Per 8 codes, 6 exp2 on the MUFU unit and 2 on the FMA pipe.
             uint32_t wd[16];
 #pragma unroll
             for (int kp = 0; kp < 4; ++kp) {
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
                     const int k = 4 * kp;
-                    const uint32_t c0 = quad_codes2(make_float2(u[4 * k + 2 * r], u[4 * k + 2 * r + 1]),
-                                                    sq[r], cr[r], false);
-                    const uint32_t c1 = quad_codes2(make_float2(u[4 * (k + 1) + 2 * r], u[4 * (k + 1) + 2 * r + 1]),
-                                                    sq[r], cr[r], false);
-                    const uint32_t c2 = quad_codes2(make_float2(u[4 * (k + 2) + 2 * r], u[4 * (k + 2) + 2 * r + 1]),
-                                                    sq[r], cr[r], false);
-                    const uint32_t c3 = quad_codes2(make_float2(u[4 * (k + 3) + 2 * r], u[4 * (k + 3) + 2 * r + 1]),
-                                                    sq[r], cr[r], true);
-                    wd[4 * kp + 2 * r] = c0 | (c1 << 16);
-                    wd[4 * kp + 2 * r + 1] = c2 | (c3 << 16);
+                    const float2 c0 = quad_round2(make_float2(u[4 * k + 2 * r], u[4 * k + 2 * r + 1]),
+                                                  sq[r], cr[r], false);
+                    const float2 c1 = quad_round2(make_float2(u[4 * (k + 1) + 2 * r], u[4 * (k + 1) + 2 * r + 1]),
+                                                  sq[r], cr[r], IFA_QUAD_POLY >= 3);
+                    const float2 c2 = quad_round2(make_float2(u[4 * (k + 2) + 2 * r], u[4 * (k + 2) + 2 * r + 1]),
+                                                  sq[r], cr[r], IFA_QUAD_POLY >= 2);
+                    const float2 c3 = quad_round2(make_float2(u[4 * (k + 3) + 2 * r], u[4 * (k + 3) + 2 * r + 1]),
+                                                  sq[r], cr[r], IFA_QUAD_POLY >= 1);
+                    wd[4 * kp + 2 * r] = pack4(c0, c1);
+                    wd[4 * kp + 2 * r + 1] = pack4(c2, c3);
                 }
             }
             tmem_st_16x256b_x4(t_base + T_P0 + 32 * (pi & 1), wd);
-            // fold the previous block's P.V: acc = acc*alpha + float(PV)
-            if (pend) {
-                bar_wait(b_pv_full, bi & 1);
-                tc_fence_after();
-                uint32_t rs[4];
-                tmem_ld_16x256b<4>(t_base + T_RS, rs);
-#pragma unroll
-                for (int ch = 0; ch < D / 32; ++ch) {
-                    uint32_t pv[16];
-                    tmem_ld_16x256b<16>(t_base + T_PV + 32 * ch, pv);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-#pragma unroll
-                        for (int r = 0; r < 2; ++r) {
-                            const int a = 8 * ch + 2 * k;  // pair index within acc[r]
-                            const float2 pf = make_float2(__int2float_rn(static_cast<int32_t>(pv[4 * k + 2 * r])),
-                                                          __int2float_rn(static_cast<int32_t>(pv[4 * k + 2 * r + 1])));
-                            const float2 o = ffma2(make_float2(acc[r][a], acc[r][a + 1]), f2(alpha[r]), pf);
-                            acc[r][a] = o.x;
-                            acc[r][a + 1] = o.y;
-                        }
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) bar_arrive(b_pv_empty);
-                ++bi;
-#pragma unroll
-                for (int r = 0; r < 2; ++r)
-                    l[r] = __fmaf_rn(l[r], alpha[r],
-                                     static_cast<float>(static_cast<int32_t>(rs[2 * r])));
+            if (pend) {  // fold the previous block's P.V
+                fold();
                 pend = false;
             }
             tmem_wait_st();
@@ -613,48 +630,18 @@ __device__ __forceinline__ void softmax_quad(Smem<D>& sm, const Params& p, uint3
             ++i;
         }
         // last block's fold, then O = acc * (sV / l)
-        bar_wait(b_pv_full, bi & 1);
-        tc_fence_after();
-        uint32_t rs[4];
-        tmem_ld_16x256b<4>(t_base + T_RS, rs);
+        fold();
         const float sv = p.sv[w.slice];
-        float f[2];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            tmem_wait_ld();
-            l[r] = __fmaf_rn(l[r], alpha[r], static_cast<float>(static_cast<int32_t>(rs[2 * r])));
-            f[r] = __fdiv_rn(sv, l[r]);
-        }
-#pragma unroll
-        for (int ch = 0; ch < D / 32; ++ch) {
-            uint32_t pv[16];
-            tmem_ld_16x256b<16>(t_base + T_PV + 32 * ch, pv);
-            tmem_wait_ld();
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-#pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    const int a = 8 * ch + 2 * k;
-                    const float2 pf = make_float2(__int2float_rn(static_cast<int32_t>(pv[4 * k + 2 * r])),
-                                                  __int2float_rn(static_cast<int32_t>(pv[4 * k + 2 * r + 1])));
-                    const float2 o = ffma2(make_float2(acc[r][a], acc[r][a + 1]), f2(alpha[r]), pf);
-                    acc[r][a] = o.x;
-                    acc[r][a + 1] = o.y;
-                }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) bar_arrive(b_pv_empty);
-        ++bi;
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             if (grow[r] >= n) continue;
+            const float f = __fdiv_rn(sv, l[r]);
             float* orow = p.o + (static_cast<int64_t>(w.slice) * n + grow[r]) * p.d;
 #pragma unroll
             for (int k = 0; k < D / 8; ++k) {
                 const int col = 8 * k + 2 * static_cast<int>(t0);
                 if (col < p.d) {
-                    const float2 o = make_float2(acc[r][2 * k] * f[r], acc[r][2 * k + 1] * f[r]);
+                    const float2 o = make_float2(acc[r][2 * k] * f, acc[r][2 * k + 1] * f);
                     if (col + 1 < p.d)
                         __stcs(reinterpret_cast<float2*>(orow + col), o);
                     else
@@ -1143,7 +1130,6 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
                 const int32_t d = p.d;
                 float* orow = p.o + (static_cast<int64_t>(w.slice) * n + grow) * d + c_base;
                 float out[NCOL];
-#pragma unroll
                 if constexpr (FAST) {
                     const float f = __fdiv_rn(sv, l);
 #pragma unroll
