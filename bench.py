@@ -148,6 +148,40 @@ def measure_int8_peak(torch, dev) -> dict:
         return {"tops": 4500.0, "source": "nominal B200 dense INT8 (4.5 POPS)"}
 
 
+def half_int8_timing(torch, plan, v, slices, n, d, ops, stream, steps) -> dict:
+    """SURVEY §8(f) f1 on the same inputs: the half-INT8 kernel (int8 Q/K
+    from the plan, fp16 copy of the f32 V) timed alone, plus the V -> fp16
+    conversion it needs."""
+    from paper_2409_16997_b200 import _lib
+    lib = _lib.load()
+    vh = torch.empty(v.shape, dtype=torch.float16, device=v.device)
+    out = torch.empty(v.shape, dtype=torch.float32, device=v.device)
+    sp = stream.cuda_stream
+
+    def conv():
+        _lib.check(lib.ifa_convert_f16(v.data_ptr(), v.numel(), vh.data_ptr(), sp))
+
+    def fwd():
+        _lib.check(lib.ifa_half_int8_fwd(plan.qc.data_ptr(), plan.sq.data_ptr(),
+                                         plan.kc.data_ptr(), plan.sk.data_ptr(), vh.data_ptr(),
+                                         out.data_ptr(), slices, n, d, 128, 128, 0, sp))
+
+    res = {}
+    for name, fn in (("convert_v_ms", conv), ("attention_ms", fwd)):
+        for _ in range(2):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        res[name] = e0.elapsed_time(e1) / steps
+    res["attention_tops"] = ops / (res["attention_ms"] / 1e3) / 1e12
+    res["kernel"] = "half_int8_fwd_kernel (int8 S, fp16 P.V, f32 accumulate)"
+    return res
+
+
 def fp16_sdpa_baseline(torch, dev, slices, n, d, causal, steps=5) -> dict:
     """FlashAttention FP16/BF16 on the same GPU and shape (torch SDPA)."""
     import torch.nn.functional as F
@@ -507,6 +541,12 @@ def main() -> None:
             line["parity_spot_check"] = check
         except Exception as e:  # pragma: no cover
             line["cpu_baseline"] = {"error": str(e)[:200]}
+        if not causal:
+            try:
+                line["half_int8"] = half_int8_timing(torch, plan, v, slices, N, d, ops_rank,
+                                                     stream, max(3, args.steps // 2))
+            except Exception as e:  # pragma: no cover
+                line["half_int8"] = {"error": str(e)[:200]}
         try:
             line["fp16_flash_baseline"] = fp16_sdpa_baseline(torch, dev, slices, N, d, causal)
         except Exception as e:  # pragma: no cover

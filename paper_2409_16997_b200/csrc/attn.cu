@@ -466,17 +466,20 @@ __device__ __forceinline__ void softmax_quad(Smem<D>& sm, const Params& p, uint3
         bool pend = false;
 
         // acc = acc*alpha + float(PV), l = l*alpha + rowsum for the finished
-        // block; all TMEM loads in flight before one wait.
-        auto fold = [&]() {
+        // block: fold_issue() puts every TMEM load in flight, fold_finish()
+        // waits once and does the arithmetic.
+        uint32_t rs[4];
+        uint32_t pv[D / 2];
+        auto fold_issue = [&]() {
             bar_wait(b_pv_full, bi & 1);
             tc_fence_after();
-            uint32_t rs[4];
-            uint32_t pv[D / 2];
             tmem_ld_16x256b<4>(t_base + T_RS, rs);
 #pragma unroll
             for (int ch = 0; ch < D / 32; ++ch)
                 tmem_ld_16x256b<16>(t_base + T_PV + 32 * ch,
                                     *reinterpret_cast<uint32_t(*)[16]>(&pv[16 * ch]));
+        };
+        auto fold_finish = [&]() {
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
@@ -610,8 +613,10 @@ __device__ __forceinline__ void softmax_quad(Smem<D>& sm, const Params& p, uint3
                 }
             }
             tmem_st_16x256b_x4(t_base + T_P0 + 32 * (pi & 1), wd);
-            if (pend) {  // fold the previous block's P.V
-                fold();
+            if (pend) {  // fold the previous block's P.V (loading it before the codes
+                         // overlaps the TMEM latency but spills: measured slower)
+                fold_issue();
+                fold_finish();
                 pend = false;
             }
             tmem_wait_st();
@@ -630,7 +635,8 @@ __device__ __forceinline__ void softmax_quad(Smem<D>& sm, const Params& p, uint3
             ++i;
         }
         // last block's fold, then O = acc * (sV / l)
-        fold();
+        fold_issue();
+        fold_finish();
         const float sv = p.sv[w.slice];
 #pragma unroll
         for (int r = 0; r < 2; ++r) {

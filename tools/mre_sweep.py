@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""C4 accuracy sweep on the GPU: MRE of the full-INT8 forward against the
+"""C4 accuracy sweep on the GPU: MRE of the full-INT8 forward (exact and
+tolerance mode) and of the half-INT8 forward against the
 fp64 reference attention, N = 1k..16k, d = 128, normal and uniform
 activations, with and without outlier tokens (BASELINE.json configs[3]).
 
@@ -35,6 +36,11 @@ APPENDIX_B = {
     "normal": {1024: 2.68, 2048: 2.93, 4096: 3.06, 8192: 3.15, 16384: 3.19},
     "uniform": {1024: 1.83, 2048: 2.11, 4096: 2.57, 8192: 3.04, 16384: 3.45},
 }
+# reference half-INT8 MRE vs fp64 (same inputs).
+APPENDIX_B_HALF = {
+    "normal": {1024: 2.01, 2048: 2.30, 4096: 2.41, 8192: 2.52, 16384: 2.56},
+    "uniform": {1024: 0.496, 2048: 0.498, 4096: 0.514, 8192: 0.523, 16384: 0.514},
+}
 # Paper tables (RTX 4090, Triton; shape details unstated): PAPER.md:163-187.
 PAPER = {
     "normal": {1024: 4.05, 2048: 4.18, 4096: 4.21, 8192: 4.38, 16384: 4.52},
@@ -49,6 +55,13 @@ def int8_forward(q, k, v, bc, fast):
     vq = ifa.quantize_per_tensor(dev(v))
     cfg = ifa.AttentionConfig(ifa.BlockSpec(128, bc), fast=fast)
     return ifa.int_flash_attention(ifa.QuantizedAttentionInputs(qq, kq, vq), cfg)
+
+
+def half_forward(q, k, v):
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    qq = ifa.quantize_per_row(dev(q))
+    kq = ifa.quantize_per_row(dev(k))
+    return ifa.half_int8_attention(qq, kq, dev(v), ifa.AttentionConfig(ifa.BlockSpec(128, 128)))
 
 
 def run_case(o, dist, n, d, seed_idx, outlier=None):
@@ -66,6 +79,9 @@ def run_case(o, dist, n, d, seed_idx, outlier=None):
         acc = ErrorAccum()
         acc.add(ref, out)
         res[mode] = acc
+    acc = ErrorAccum()
+    acc.add(ref, half_forward(q, k, v))
+    res["half"] = acc
     return res
 
 
@@ -85,20 +101,22 @@ def main():
             rows.append({"dist": dist, "n": n, "outliers": "none",
                          "mre_exact_pct": 100 * r["exact"].ratio(),
                          "mre_fast_pct": 100 * r["fast"].ratio(),
-                         "appendix_b_pct": APPENDIX_B[dist][n], "paper_pct": PAPER[dist][n]})
+                         "mre_half_pct": 100 * r["half"].ratio(),
+                         "appendix_b_pct": APPENDIX_B[dist][n], "paper_pct": PAPER[dist][n],
+                         "appendix_b_half_pct": APPENDIX_B_HALF[dist][n]})
     settings = [("x10 in Q,K,V", (10.0, (0, 1, 2))), ("x100 in Q,K,V", (100.0, (0, 1, 2))),
                 ("x10 in Q,K only", (10.0, (0, 1))), ("x10 in V only", (10.0, (2,)))]
     for dist in ("normal", "uniform"):
         for label, spec in settings:
-            accs = {"exact": ErrorAccum(), "fast": ErrorAccum()}
-            per_seed = {"exact": [], "fast": []}
+            per_seed = {"exact": [], "fast": [], "half": []}
             for seed_idx in (21, 22, 23):
                 r = run_case(o, dist, 1024, d, seed_idx, outlier=spec)
-                for m in accs:
+                for m in per_seed:
                     per_seed[m].append(r[m].ratio())
             rows.append({"dist": dist, "n": 1024, "outliers": label,
                          "mre_exact_pct": 100 * float(np.mean(per_seed["exact"])),
-                         "mre_fast_pct": 100 * float(np.mean(per_seed["fast"]))})
+                         "mre_fast_pct": 100 * float(np.mean(per_seed["fast"])),
+                         "mre_half_pct": 100 * float(np.mean(per_seed["half"]))})
     wall = time.time() - t0
     with open(args.out + ".json", "w") as f:
         json.dump({"rows": rows, "wall_s": wall, "d": d, "bc": 128,
@@ -106,12 +124,14 @@ def main():
                    "outlier_definition": "paper_2409_16997_b200.evaluation.inject_outliers "
                                          "(1% of rows, PCG64 partial Fisher-Yates)"}, f,
                   indent=1)
-    lines = ["| dist | N | outliers | MRE exact (%) | MRE fast (%) | reference, Appendix B (%) "
-             "| paper, RTX 4090 (%) |", "|---|---|---|---|---|---|---|"]
+    lines = ["| dist | N | outliers | full-INT8 exact (%) | full-INT8 fast (%) | "
+             "reference full-INT8, App. B (%) | paper full-INT8, RTX 4090 (%) | half-INT8 (%) | "
+             "reference half-INT8, App. B (%) |", "|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         lines.append(f"| {r['dist']} | {r['n']} | {r['outliers']} | {r['mre_exact_pct']:.3f} | "
                      f"{r['mre_fast_pct']:.3f} | {r.get('appendix_b_pct', '')} | "
-                     f"{r.get('paper_pct', '')} |")
+                     f"{r.get('paper_pct', '')} | {r['mre_half_pct']:.3f} | "
+                     f"{r.get('appendix_b_half_pct', '')} |")
     with open(args.out + ".md", "w") as f:
         f.write("\n".join(lines) + f"\n\nwall {wall:.1f} s on one B200\n")
     print("\n".join(lines))
