@@ -469,7 +469,8 @@ def main() -> None:
             "bound": "tensor", "achieved": achieved, "peak": peak["tops"], "unit": "TOPS",
             "frac": achieved / peak["tops"], "traffic": traffic,
             "peak_source": peak["source"], "frac_of_nominal_4500": achieved / 4500.0,
-            "kernel": "int_flash_fwd_kernel (CUDA events around each launch)",
+            "kernel": ("int_flash_pp_kernel + V fp16 conversion" if plan.uses_pp_kernel()
+                       else "int_flash_fwd_kernel") + " (CUDA events around each launch)",
             "algorithmic_ops_per_launch": ops_rank,
         }
         hbm = load_peaks().get("hbm_gbs") or 6650.0

@@ -1,0 +1,696 @@
+// attn_pp.cu -- tolerance-mode INT-FlashAttention forward with two Q tiles
+// per CTA in ping-pong (IFA_FLAG_FAST, non-causal, every KV block one
+// 128-key tile).  Same algorithm as attention.cpp:235-357 per block: exact
+// int32 S = Q.K^T (tcgen05.mma kind::i8), dequantize, running row max,
+// requantize P to integer codes round(127 * exp(s - m)), O = O*alpha + P.V,
+// l = l*alpha + sum(codes), O * sV / l at the end.
+//
+// What differs from the one-tile kernels in attn.cu is where O lives.  The
+// P codes (0..127) and V codes (-127..127) are exact in fp16, their products
+// (<= 127^2) and 128-key sums (< 2^21) exact in f32, so P.V can run as
+// tcgen05.mma kind::f16 accumulating straight into an f32 O in TMEM: the
+// tensor core performs the fold's "+ float(PV)".  The softmax warps only
+// rescale the O rows whose running max moved (alpha != 1), reading and
+// writing TMEM, and no longer hold a 128-column accumulator in registers.
+// That frees the register file for a second 128-row Q tile: 16 math warps in
+// two groups of 8 (quad layout: 16 TMEM lanes x 128 columns per warp, two
+// rows x 32 keys per thread), four math warps per SM sub-partition.
+//
+// TMEM (512 columns): group g uses S [256g, 256g+128) and O [256g+128,
+// 256g+128+D).  S(j+1) of a group is issued as soon as the group has read
+// S(j), so the tensor core computes the next scores while the softmax works.
+// P goes to shared memory (fp16, K-major, 128B swizzle; 32 KiB per group)
+// and P.V(j) reads it from there; the group waits for P.V(j-1) (which also
+// makes O(j-1) final) before it rescales O and overwrites P.
+//
+// Each thread writes its row's 32 keys (8k + 2t0 + e, k = 0..15) as 64
+// contiguous bytes, i.e. MMA keys [32 t0, 32 t0 + 32) in order 2k + e; the
+// fp16 V tile is loaded with its rows permuted the same way (smem row
+// 32t + 2k + e <- key 8k + 2t + e) by a 5-D tensor map.  Needs n % 128 == 0.
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "ifa_internal.h"
+#include "ptx.cuh"
+
+namespace ifa_b200 {
+namespace pp {
+
+using namespace ptx;
+
+constexpr int BM = 128;
+constexpr int BN = 128;
+constexpr int KST = 3;  // K tiles (+ K scales) in flight
+constexpr int VST = 2;  // fp16 V tiles in flight
+constexpr int CTRL_WARPS = 4;
+constexpr int GROUP_WARPS = 8;
+constexpr int NUM_THREADS = 32 * (CTRL_WARPS + 2 * GROUP_WARPS);
+constexpr uint32_t kRegsControl = 32;
+// setmaxnreg moves registers inside the CTA pool allocated at launch (640 x 96
+// = 61440): 4*32*32 + 16*32*112 = 61440.
+constexpr uint32_t kRegsMath = 112;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+constexpr float kLog2_127 = 6.9886846867721655f;
+constexpr float kLog2e = 1.4426950408889634f;
+
+template <int D>
+struct alignas(1024) Smem {
+    uint8_t q[2][BM * D];            // [group]
+    uint8_t k[KST][BN * D];
+    uint8_t v[VST][BN * D * 2];      // fp16 codes: [D/64 halves][BN permuted rows][64]
+    uint8_t p[2][BM * BN * 2];       // [group] fp16 P, K-major SW128: 2 K-atoms of 64 keys
+    float sk[KST][BN];
+    uint64_t q_full, q_empty;
+    uint64_t k_full[KST], k_empty[KST], v_full[VST], v_empty[VST];
+    uint64_t s_full[2], s_empty[2], p_full[2], p_empty[2], o_full[2], o_free[2];
+    uint32_t tmem_base;
+};
+
+struct Params {
+    const float* sq;
+    const float* sk;
+    const float* sv;
+    float* o;
+    int32_t n, d;
+    float sk_mul;  // log2(e) [* 1/sqrt(d)]: scores are kept in the log2 domain
+    int32_t pairs, slices, items;
+};
+
+template <int N>
+struct Ring {
+    uint32_t idx = 0, phase = 0;
+    __device__ __forceinline__ void advance() {
+        if (++idx == N) {
+            idx = 0;
+            phase ^= 1u;
+        }
+    }
+};
+
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+__device__ __forceinline__ float ex2(float t) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(t));
+    return r;
+}
+
+// 2^t on the FMA pipe (degree-5 polynomial, 3.5e-7 relative), t clamped at -64.
+__device__ __forceinline__ float2 exp2_poly2(float2 t) {
+    t.x = fmaxf(t.x, -64.0f);
+    t.y = fmaxf(t.y, -64.0f);
+    const float2 r = fadd2(t, f2(kMagic));
+    const float2 f = fsub2(t, fsub2(r, f2(kMagic)));
+    float2 y = ffma2(f, f2(1.2915651313960552e-3f), f2(9.668535552918911e-3f));
+    y = ffma2(y, f, f2(5.5516887456178665e-2f));
+    y = ffma2(y, f, f2(2.4022264778614044e-1f));
+    y = ffma2(y, f, f2(6.931464672088623e-1f));
+    y = ffma2(y, f, f2(1.0f));
+    return make_float2(__int_as_float(__float_as_int(y.x) + (__float_as_int(r.x) << 23)),
+                       __int_as_float(__float_as_int(y.y) + (__float_as_int(r.y) << 23)));
+}
+
+__device__ __forceinline__ void ld16x256_x4(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void st16x256_x4(uint32_t taddr, const uint32_t* r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+        "r"(r[15])
+        : "memory");
+}
+
+// kind::f16 instruction descriptor: D=F32, A=B=F16, A K-major.
+__host__ __device__ constexpr uint32_t idesc_f16(uint32_t m, uint32_t n, bool b_mn_major) {
+    return (1u << 4) | ((b_mn_major ? 1u : 0u) << 16) | ((n >> 3) << 17) | ((m >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    int_flash_pp_kernel(const __grid_constant__ CUtensorMap tm_q,
+                        const __grid_constant__ CUtensorMap tm_k,
+                        const __grid_constant__ CUtensorMap tm_v, const Params p) {
+    constexpr uint32_t kLayout = D == 128 ? kLayoutSw128 : kLayoutSw64;
+    constexpr uint32_t kSbo = 8 * D;
+    constexpr uint32_t kIdescS = idesc_i8(BM, BN, false, false);
+    constexpr uint32_t kIdescPV = idesc_f16(BM, D, true);
+
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    Smem<D>& sm = *reinterpret_cast<Smem<D>*>(smem_raw);
+    const uint32_t warp = warp_id();
+    const uint32_t lane = lane_id();
+    const int32_t n = p.n;
+    const int32_t J = n / BN;  // KV tiles per item (n % 128 == 0)
+
+    const uint32_t b_q_full = smem_u32(&sm.q_full), b_q_empty = smem_u32(&sm.q_empty);
+    const uint32_t b_k_full = smem_u32(&sm.k_full[0]), b_k_empty = smem_u32(&sm.k_empty[0]);
+    const uint32_t b_v_full = smem_u32(&sm.v_full[0]), b_v_empty = smem_u32(&sm.v_empty[0]);
+    const uint32_t b_s_full = smem_u32(&sm.s_full[0]), b_s_empty = smem_u32(&sm.s_empty[0]);
+    const uint32_t b_p_full = smem_u32(&sm.p_full[0]), b_p_empty = smem_u32(&sm.p_empty[0]);
+    const uint32_t b_o_full = smem_u32(&sm.o_full[0]), b_o_free = smem_u32(&sm.o_free[0]);
+
+    if (threadIdx.x == 0) {
+        if (smem_u32(smem_raw) & 1023) __trap();
+        mbar_init(&sm.q_full, 1);
+        mbar_init(&sm.q_empty, 2);  // both MMA issuers
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&sm.s_full[i], 1);
+            mbar_init(&sm.s_empty[i], GROUP_WARPS);
+            mbar_init(&sm.p_full[i], GROUP_WARPS);
+            mbar_init(&sm.p_empty[i], 1);
+            mbar_init(&sm.o_full[i], 1);
+            mbar_init(&sm.o_free[i], GROUP_WARPS);
+        }
+        for (int i = 0; i < KST; ++i) {
+            mbar_init(&sm.k_full[i], 32);
+            mbar_init(&sm.k_empty[i], 2 + 2 * GROUP_WARPS);  // 2 MMA issuers + sK readers
+        }
+        for (int i = 0; i < VST; ++i) {
+            mbar_init(&sm.v_full[i], 1);
+            mbar_init(&sm.v_empty[i], 2);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<TMEM_COLS>(&sm.tmem_base);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem_base;
+
+    if (warp < CTRL_WARPS) {
+        regs_dealloc<kRegsControl>();
+        if (warp == 0) {
+            // ------------------------------------------------------- producer
+            const uint64_t pol_stream = policy_evict_first();
+            const uint64_t pol_keep = policy_evict_last();
+            if (lane == 0) {
+                tma_prefetch_desc(&tm_q);
+                tma_prefetch_desc(&tm_k);
+                tma_prefetch_desc(&tm_v);
+            }
+            Ring<KST> kr;
+            Ring<VST> vr;
+            uint32_t i = 0, wi = 0;
+            for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x, ++wi) {
+                const int32_t q0 = (idx % p.pairs) * 2 * BM, slice = idx / p.pairs;
+                if (lane == 0) {
+                    if (wi >= 1) bar_wait(b_q_empty, (wi - 1) & 1);
+                    mbar_arrive_expect_tx(&sm.q_full, 2 * BM * D);
+                    tma_load_3d(sm.q[0], &tm_q, &sm.q_full, 0, q0, slice, pol_stream);
+                    tma_load_3d(sm.q[1], &tm_q, &sm.q_full, 0, q0 + BM, slice, pol_stream);
+                }
+                const float* sk_slice = p.sk + static_cast<int64_t>(slice) * n;
+                for (int32_t key0 = 0; key0 < n; key0 += BN) {
+                    const uint32_t ks = kr.idx, vs = vr.idx;
+                    if (i >= KST) bar_wait(b_k_empty + 8 * ks, kr.phase ^ 1u);
+                    float4 k4 = __ldg(reinterpret_cast<const float4*>(sk_slice + key0) + lane);
+                    k4.x *= p.sk_mul;
+                    k4.y *= p.sk_mul;
+                    k4.z *= p.sk_mul;
+                    k4.w *= p.sk_mul;
+                    reinterpret_cast<float4*>(sm.sk[ks])[lane] = k4;
+                    if (lane == 0) {
+                        mbar_arrive_expect_tx(&sm.k_full[ks], BN * D);
+                        tma_load_3d(sm.k[ks], &tm_k, &sm.k_full[ks], 0, key0, slice, pol_keep);
+                        if (i >= VST) bar_wait(b_v_empty + 8 * vs, vr.phase ^ 1u);
+                        mbar_arrive_expect_tx(&sm.v_full[vs], BN * D * 2);
+                        const int32_t tile = (slice * n + key0) / BN;
+#pragma unroll
+                        for (int h = 0; h < D / 64; ++h)
+                            tma_load_5d(sm.v[vs] + h * BN * 128, &tm_v, &sm.v_full[vs], 64 * h,
+                                        0, 0, 0, tile, pol_keep);
+                    } else {
+                        bar_arrive(b_k_full + 8 * ks);
+                    }
+                    kr.advance();
+                    vr.advance();
+                    ++i;
+                }
+            }
+        } else if (warp == 1 || warp == 2) {
+            // ------------------------------------------- MMA issuers (one per group)
+            // Warp 1 issues group 0's MMAs, warp 2 group 1's, so neither group
+            // waits on the other's progress.  Per block j: S(next) as soon as the
+            // group has read S(j), then P.V(j) once it has published P(j).
+            if (lane == 0) {
+                const int g = static_cast<int>(warp) - 1;
+                Ring<KST> kr;     // K stage of block j
+                Ring<VST> vr;     // V stage of block j
+                uint32_t t = 0;   // tiles of this group so far
+                uint32_t wi = 0;
+                const uint32_t d_s = tmem + 256 * g, d_o = d_s + 128;
+                auto issue_s = [&](uint32_t ks, uint32_t kph) {
+                    bar_wait(b_k_full + 8 * ks, kph);
+                    tc_fence_after();
+                    const uint32_t q_base = smem_u32(sm.q[g]);
+                    const uint32_t k_base = smem_u32(sm.k[ks]);
+#pragma unroll
+                    for (int kk = 0; kk < D / 32; ++kk) {
+                        const uint64_t adesc = smem_desc(q_base + kk * 32, 16, kSbo, kLayout);
+                        const uint64_t bdesc = smem_desc(k_base + kk * 32, 16, kSbo, kLayout);
+                        mma_i8_ss(d_s, adesc, bdesc, kIdescS, kk > 0 ? 1u : 0u);
+                    }
+                    mma_commit_u32(b_s_full + 8 * g);
+                };
+                if (blockIdx.x < p.items) {
+                    bar_wait(b_q_full, 0);
+                    issue_s(0, 0);
+                }
+                const uint32_t p_base = smem_u32(sm.p[g]);
+                for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x, ++wi) {
+                    const bool has_next_item = idx + static_cast<int32_t>(gridDim.x) < p.items;
+                    for (int32_t j = 0; j < J; ++j, ++t) {
+                        Ring<KST> nk = kr;
+                        nk.advance();
+                        const bool last = j == J - 1;
+                        mma_commit_u32(b_k_empty + 8 * kr.idx);  // S(j) issued
+                        if (last) {
+                            mma_commit_u32(b_q_empty);  // every S of this item issued
+                            if (has_next_item) bar_wait(b_q_full, (wi + 1) & 1);
+                        }
+                        if (!last || has_next_item) {
+                            bar_wait(b_s_empty + 8 * g, t & 1);
+                            issue_s(nk.idx, nk.phase);
+                        }
+                        bar_wait(b_v_full + 8 * vr.idx, vr.phase);
+                        const uint32_t v_base = smem_u32(sm.v[vr.idx]);
+                        bar_wait(b_p_full + 8 * g, t & 1);
+                        if (j == 0 && wi > 0) bar_wait(b_o_free + 8 * g, (wi - 1) & 1);
+                        tc_fence_after();
+#pragma unroll
+                        for (int kk = 0; kk < BN / 16; ++kk) {
+                            const uint64_t adesc = smem_desc(
+                                p_base + (kk >> 2) * (BM * 128) + (kk & 3) * 32, 16, 1024,
+                                kLayoutSw128);
+                            const uint64_t bdesc =
+                                smem_desc(v_base + kk * 16 * 128, BN * 128, 1024, kLayoutSw128);
+                            mma_f16_ss(d_o, adesc, bdesc, kIdescPV, (j == 0 && kk == 0) ? 0u : 1u);
+                        }
+                        mma_commit_u32(b_p_empty + 8 * g);
+                        if (last) mma_commit_u32(b_o_full + 8 * g);
+                        mma_commit_u32(b_v_empty + 8 * vr.idx);
+                        kr.advance();
+                        vr.advance();
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    } else {
+        regs_alloc<kRegsMath>();
+        // -------------------------------------------- softmax + correction
+        const uint32_t mw = warp - CTRL_WARPS;
+        const uint32_t g = mw >> 3;                 // Q tile / group
+        const uint32_t quarter = warp & 3;          // TMEM lane quarter of this warp
+        const uint32_t half = (mw >> 2) & 1;        // which 16 lanes of the quarter
+        const uint32_t t0 = lane & 3;
+        const uint32_t lane_base = quarter * 32 + half * 16;
+        const int32_t row0 = static_cast<int32_t>(lane_base + (lane >> 2));  // and row0 + 8
+        const uint32_t t_s = tmem + (lane_base << 16) + 256 * g;  // S
+        const uint32_t t_o = t_s + 128;                            // O
+        const uint32_t bs_full = b_s_full + 8 * g, bs_empty = b_s_empty + 8 * g;
+        const uint32_t bp_full = b_p_full + 8 * g, bp_empty = b_p_empty + 8 * g;
+        const uint32_t bo_full = b_o_full + 8 * g, bo_free = b_o_free + 8 * g;
+        // P (fp16, K-major SW128): row r, MMA keys [32 t0, 32 t0 + 32) = 64 bytes =
+        // chunks 4 (t0 & 1) .. +3 of K-atom t0 >> 1, XOR-swizzled by r & 7.
+        uint32_t p_row[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const uint32_t row = static_cast<uint32_t>(row0) + 8 * r;
+            p_row[r] = smem_u32(sm.p[g]) + (t0 >> 1) * (BM * 128) + row * 128;
+        }
+        const uint32_t sw = static_cast<uint32_t>(row0) & 7;  // same for row0 + 8
+        Ring<KST> kv;
+        uint32_t tc = 0, wi = 0;
+
+        for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x, ++wi) {
+            const int32_t q0 = (idx % p.pairs) * 2 * BM + static_cast<int32_t>(g) * BM;
+            const int32_t slice = idx / p.pairs;
+            int32_t grow[2];
+            float sq[2];
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                grow[r] = q0 + row0 + 8 * r;
+                sq[r] = grow[r] < n ? p.sq[static_cast<int64_t>(slice) * n + grow[r]] : 0.0f;
+            }
+            float l[2] = {0.0f, 0.0f}, m[2] = {-__int_as_float(0x7f800000), -__int_as_float(0x7f800000)};
+
+            for (int32_t j = 0; j < J; ++j, ++tc) {
+                const uint32_t st = kv.idx;
+                bar_wait(bs_full, tc & 1);
+                tc_fence_after();
+                uint32_t sr[64];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) ld16x256_x4(t_s + 32 * c, &sr[16 * c]);
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) bar_arrive(bs_empty);
+                bar_wait(b_k_full + 8 * st, kv.phase);
+                // u = float(S) * sK * log2(e); sr[4k + {0,1}] row0, [4k + {2,3}] row1,
+                // keys 8k + 2*t0 + {0,1}
+                float u[64];
+                const float* skc = sm.sk[st] + 2 * t0;
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const float2 s2 = *reinterpret_cast<const float2*>(skc + 8 * k);
+                    const float2 a = fmul2(make_float2(__int2float_rn(static_cast<int32_t>(sr[4 * k])),
+                                                       __int2float_rn(static_cast<int32_t>(sr[4 * k + 1]))),
+                                           s2);
+                    const float2 b = fmul2(make_float2(__int2float_rn(static_cast<int32_t>(sr[4 * k + 2])),
+                                                       __int2float_rn(static_cast<int32_t>(sr[4 * k + 3]))),
+                                           s2);
+                    u[4 * k] = a.x;
+                    u[4 * k + 1] = a.y;
+                    u[4 * k + 2] = b.x;
+                    u[4 * k + 3] = b.y;
+                }
+                __syncwarp();
+                if (lane == 0) bar_arrive(b_k_empty + 8 * st);
+                float cr[2], alpha[2];
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    float a[11];
+#pragma unroll
+                    for (int jj = 0; jj < 10; ++jj) {
+                        const int v0 = 3 * jj, v1 = 3 * jj + 1, v2 = 3 * jj + 2;
+                        a[jj] = fmax3(u[4 * (v0 >> 1) + 2 * r + (v0 & 1)],
+                                      u[4 * (v1 >> 1) + 2 * r + (v1 & 1)],
+                                      u[4 * (v2 >> 1) + 2 * r + (v2 & 1)]);
+                    }
+                    a[10] = fmaxf(u[4 * 15 + 2 * r], u[4 * 15 + 2 * r + 1]);
+                    float b = fmaxf(fmax3(fmax3(a[0], a[1], a[2]), fmax3(a[3], a[4], a[5]),
+                                          fmax3(a[6], a[7], a[8])),
+                                    fmaxf(a[9], a[10]));
+                    b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, 1));
+                    b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, 2));
+                    const float mnew = (m[r] < b) ? b : m[r];
+                    cr[r] = kLog2_127 - sq[r] * mnew;
+                    alpha[r] = (j == 0 || mnew == m[r]) ? 1.0f : ex2(sq[r] * (m[r] - mnew));
+                    m[r] = mnew;
+                }
+                // codes: round(2^t) as exact fp16 integers; 6 of 8 exp2 on MUFU,
+                // 2 on the FMA pipe.  wd[r][k] = keys (8k + 2t0, +1) of row r.
+                uint32_t wd[2][16];
+                float2 ls[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        const float2 t = ffma2(make_float2(u[4 * k + 2 * r], u[4 * k + 2 * r + 1]),
+                                               f2(sq[r]), f2(cr[r]));
+                        const float2 y = (k & 3) == 3 ? exp2_poly2(t)
+                                                      : make_float2(ex2(t.x), ex2(t.y));
+                        const float2 c = fsub2(fadd2(y, f2(kMagic)), f2(kMagic));
+                        ls[r] = fadd2(ls[r], c);
+                        const __half2 h = __floats2half2_rn(c.x, c.y);
+                        wd[r][k] = *reinterpret_cast<const uint32_t*>(&h);
+                    }
+                }
+                // P.V(j-1) done: the P buffer is free and O(j-1) is final
+                if (tc > 0) bar_wait(bp_empty, (tc - 1) & 1);
+                tc_fence_after();
+                const bool need = j > 0 && (alpha[0] != 1.0f || alpha[1] != 1.0f);
+                if (__any_sync(0xffffffffu, need)) {
+#pragma unroll
+                    for (int c = 0; c < D / 32; ++c) {
+                        uint32_t o[16];
+                        ld16x256_x4(t_o + 32 * c, o);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+#pragma unroll
+                            for (int r = 0; r < 2; ++r) {
+                                const float2 v = fmul2(make_float2(__uint_as_float(o[4 * k + 2 * r]),
+                                                                   __uint_as_float(o[4 * k + 2 * r + 1])),
+                                                       f2(alpha[r]));
+                                o[4 * k + 2 * r] = __float_as_uint(v.x);
+                                o[4 * k + 2 * r + 1] = __float_as_uint(v.y);
+                            }
+                        st16x256_x4(t_o + 32 * c, o);
+                    }
+                    tmem_wait_st();
+                }
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t chunk = (4 * (t0 & 1) + i) ^ sw;
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                         p_row[r] + chunk * 16),
+                                     "r"(wd[r][4 * i]), "r"(wd[r][4 * i + 1]),
+                                     "r"(wd[r][4 * i + 2]), "r"(wd[r][4 * i + 3])
+                                     : "memory");
+                    }
+                fence_proxy_async_shared();  // P is read by the tensor core
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) bar_arrive(bp_full);
+#pragma unroll
+                for (int r = 0; r < 2; ++r) l[r] = __fmaf_rn(l[r], alpha[r], ls[r].x + ls[r].y);
+                kv.advance();
+            }
+            // epilogue: O * sV / l, l summed over the quad
+            const float sv = p.sv[slice];
+            float f[2];
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                float lt = l[r];
+                lt += __shfl_xor_sync(0xffffffffu, lt, 1);
+                lt += __shfl_xor_sync(0xffffffffu, lt, 2);
+                f[r] = __fdiv_rn(sv, lt);
+            }
+            bar_wait(bo_full, wi & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+                uint32_t o[16];
+                ld16x256_x4(t_o + 32 * c, o);
+                tmem_wait_ld();
+                if (c == D / 32 - 1) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) bar_arrive(bo_free);
+                }
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    if (grow[r] >= n) continue;
+                    float* orow = p.o + (static_cast<int64_t>(slice) * n + grow[r]) * p.d;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int col = 32 * c + 8 * k + 2 * static_cast<int>(t0);
+                        const float2 v = make_float2(__uint_as_float(o[4 * k + 2 * r]) * f[r],
+                                                     __uint_as_float(o[4 * k + 2 * r + 1]) * f[r]);
+                        if (col + 1 < p.d)
+                            __stcs(reinterpret_cast<float2*>(orow + col), v);
+                        else if (col < p.d)
+                            orow[col] = v.x;
+                    }
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<TMEM_COLS>(tmem);
+    }
+}
+
+// int8 codes [rows][pitch] -> fp16 [rows][D] (columns >= pitch are zero).
+__global__ void codes_to_f16_kernel(const int8_t* __restrict__ src, int64_t rows, int64_t pitch,
+                                    int dcols, __half* __restrict__ dst) {
+    const int64_t total = rows * dcols;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total / 8;
+         i += stride) {
+        const int64_t e = 8 * i, r = e / dcols, c = e - r * dcols;
+        __align__(16) __half h[8];
+        if (c + 8 <= pitch && (pitch % 8) == 0) {
+            const uint2 w = *reinterpret_cast<const uint2*>(src + r * pitch + c);
+            const int8_t* b = reinterpret_cast<const int8_t*>(&w);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) h[t] = __int2half_rn(b[t]);
+        } else {
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                h[t] = __int2half_rn(c + t < pitch ? src[r * pitch + c + t] : 0);
+        }
+        *reinterpret_cast<uint4*>(dst + e) = *reinterpret_cast<const uint4*>(h);
+    }
+}
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(ptr);
+    }
+    return fn;
+}
+
+// int8 codes [slices][n][pitch], box {D, 128 rows, 1 slice}
+static bool make_map_codes(CUtensorMap* map, const int8_t* base, int64_t slices, int64_t n,
+                           int64_t pitch, int D) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(pitch), static_cast<cuuint64_t>(n),
+                                static_cast<cuuint64_t>(slices)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(pitch),
+                                   static_cast<cuuint64_t>(pitch * n)};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(D), 128u, 1u};
+    const cuuint32_t estr[3] = {1u, 1u, 1u};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides,
+               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               D == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+}
+
+// fp16 V [slices*n][D] viewed as {64 cols, e:2, k:16, t:4, tile} so that
+// smem row 32t + 2k + e of a 128-key tile holds key 8k + 2t + e: the MMA key
+// order of the P rows the softmax threads write (thread t0 of a row owns MMA
+// keys [32 t0, 32 t0 + 32) = its keys 8k + 2 t0 + e).
+static bool make_map_v16(CUtensorMap* map, const __half* base, int64_t slices, int64_t n, int D) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc || n % 128 != 0) return false;
+    const cuuint64_t row = static_cast<cuuint64_t>(D) * 2;
+    const cuuint64_t dims[5] = {static_cast<cuuint64_t>(D), 2, 16, 4,
+                                static_cast<cuuint64_t>(slices * n / 128)};
+    const cuuint64_t strides[4] = {row, 8 * row, 2 * row, 128 * row};
+    const cuuint32_t box[5] = {64u, 2u, 16u, 4u, 1u};
+    const cuuint32_t estr[5] = {1u, 1u, 1u, 1u, 1u};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<__half*>(base), dims, strides,
+               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+}
+
+template <int D>
+static cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
+    static bool pool_kept = false;
+    if (!pool_kept) {  // keep the per-call fp16 V workspace in the stream-ordered pool
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        pool_kept = true;
+    }
+    __half* v16 = nullptr;
+    const int64_t rows = a.slices * a.n;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&v16), rows * D * 2, stream);
+    if (e != cudaSuccess) return e;
+    {
+        int64_t blocks = (rows * D / 8 + 255) / 256;
+        if (blocks > 148 * 16) blocks = 148 * 16;
+        codes_to_f16_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(a.v, rows, a.pitch,
+                                                                                D, v16);
+    }
+    CUtensorMap tq, tk, tv;
+    if (!make_map_codes(&tq, a.q, a.slices, a.n, a.pitch, D) ||
+        !make_map_codes(&tk, a.k, a.slices, a.n, a.pitch, D) ||
+        !make_map_v16(&tv, v16, a.slices, a.n, D)) {
+        cudaFreeAsync(v16, stream);
+        return cudaErrorInvalidValue;
+    }
+    Params p;
+    p.sq = a.sq;
+    p.sk = a.sk;
+    p.sv = a.sv;
+    p.o = a.o;
+    p.n = static_cast<int32_t>(a.n);
+    p.d = static_cast<int32_t>(a.d);
+    p.sk_mul = kLog2e * ((a.flags & IFA_FLAG_SQRT_D) ? 1.0f / sqrtf(static_cast<float>(a.d)) : 1.0f);
+    const int32_t q_tiles = static_cast<int32_t>((a.n + BM - 1) / BM);
+    p.pairs = (q_tiles + 1) / 2;
+    p.slices = static_cast<int32_t>(a.slices);
+    p.items = p.pairs * p.slices;
+    const size_t smem = sizeof(Smem<D>) + 1024;
+    static bool configured = false;
+    if (!configured) {
+        e = cudaFuncSetAttribute(int_flash_pp_kernel<D>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+        if (e != cudaSuccess) {
+            cudaFreeAsync(v16, stream);
+            return e;
+        }
+        configured = true;
+    }
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    const int grid = p.items < sms ? p.items : sms;
+    int_flash_pp_kernel<D><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+    e = cudaGetLastError();
+    const cudaError_t e2 = cudaFreeAsync(v16, stream);
+    return e != cudaSuccess ? e : e2;
+}
+
+}  // namespace pp
+
+bool int_flash_pp_eligible(const AttnArgs& a) {
+    const char* off = std::getenv("IFA_B200_NO_PP");
+    if (off && off[0] == '1') return false;
+    const int64_t bc = a.bc < a.n ? a.bc : a.n;
+    const bool tiles_are_blocks = bc == pp::BN || (bc == a.n && a.n <= pp::BN);
+    return (a.flags & IFA_FLAG_FAST) && !(a.flags & IFA_FLAG_CAUSAL) &&
+           a.audit == nullptr && tiles_are_blocks && a.n % 128 == 0 && a.d <= 128;
+}
+
+cudaError_t launch_int_flash_pp(const AttnArgs& a, cudaStream_t stream) {
+    if (a.d <= 64) return pp::launch<64>(a, stream);
+    return pp::launch<128>(a, stream);
+}
+
+}  // namespace ifa_b200

@@ -44,6 +44,11 @@ struct AttnArgs {
 // makes zero-padded copies when d % 16 != 0); columns >= d must be zero.
 cudaError_t launch_int_flash_fwd(const AttnArgs& a, cudaStream_t stream);
 
+// attn_pp.cu: tolerance-mode kernel with two Q tiles per CTA (non-causal,
+// 128-key blocks, n % 16 == 0); IFA_B200_NO_PP=1 disables it.
+bool int_flash_pp_eligible(const AttnArgs& a);
+cudaError_t launch_int_flash_pp(const AttnArgs& a, cudaStream_t stream);
+
 // attn_half.cu: half-INT8 forward (q/k codes of row pitch `pitch`, v fp16
 // [slices][n][d] dense, d in {64, 128}) and the f32 -> fp16 conversion.
 cudaError_t launch_half_int8_fwd(const int8_t* q, const float* sq, const int8_t* k,

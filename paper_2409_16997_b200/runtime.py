@@ -12,6 +12,7 @@ mirror of the reference functions.
 """
 from __future__ import annotations
 
+import os
 from typing import Optional
 
 import torch
@@ -82,13 +83,24 @@ class AttentionPlan:
         self.quantize(q, k, v, stream)
         return self.attention(stream)
 
+    def uses_pp_kernel(self) -> bool:
+        """True when ifa_int_flash_fwd takes the two-Q-tile tolerance kernel
+        (csrc/attn_pp.cu: fast mode, non-causal, Bc = 128, n % 128 == 0),
+        which first converts the V codes to fp16 (one extra launch)."""
+        bc = min(self.bc, self.n)
+        blocks = bc == 128 or (bc == self.n and self.n <= 128)
+        return bool(self.flags & _lib.FLAG_FAST) and not (self.flags & _lib.FLAG_CAUSAL) and \
+            blocks and self.n % 128 == 0 and self.d <= 128 and \
+            os.environ.get("IFA_B200_NO_PP", "") != "1"
+
     def launches_per_step(self) -> int:
         """Kernels one forward() launches (quantize: Q rows, K rows, fused V
         slices -- or absmax + quantize + a memset on shapes the fused V
-        kernel does not take; attention: one persistent kernel)."""
+        kernel does not take; attention: one persistent kernel, plus the V
+        fp16 conversion on the two-Q-tile path)."""
         elems = self.n * self.d
         v_fused = elems % 16 == 0 and self.d % 4 == 0
-        return 2 + (1 if v_fused else 3) + 1
+        return 2 + (1 if v_fused else 3) + (2 if self.uses_pp_kernel() else 1)
 
     def check(self) -> None:
         """Raise like the reference if any quantized input was non-finite."""

@@ -265,7 +265,8 @@ def _fast_close(got, want, vc, vs):
 @pytest.mark.parametrize("dist", ["normal", "uniform"])
 @pytest.mark.parametrize("causal", [False, True])
 def test_fast_mode_within_tolerance(ifa, oracle, n, d, dist, causal):
-    """n % 32 == 0 runs the quad-layout kernel (8 math warps); the others the
+    """Non-causal n % 128 == 0 runs the two-Q-tile kernel (attn_pp.cu), other
+    n % 32 == 0 shapes the quad-layout kernel (8 math warps), the rest the
     16-warp one."""
     _, (qc, qs, kc, ks, vc, vs) = _quantized_case(oracle, dist, n, d, seed=n + d)
     want = oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, 128,
@@ -304,7 +305,55 @@ def test_fast_mode_both_kernels_agree(ifa, oracle, n, d, causal, monkeypatch):
         ifa.QuantizedRows(_dev(qc), _dev(qs)), ifa.QuantizedRows(_dev(kc), _dev(ks)),
         ifa.QuantizedTensor(_dev(vc), _dev(np.asarray(vs, np.float32))))
     cfg = ifa.AttentionConfig(ifa.BlockSpec(64, 128), causal=causal, fast=True)
+    monkeypatch.setenv("IFA_B200_NO_PP", "1")
     a = ifa.int_flash_attention(inputs, cfg).cpu().numpy().astype(np.float64)
     monkeypatch.setenv("IFA_B200_NO_QUAD", "1")
     b = ifa.int_flash_attention(inputs, cfg).cpu().numpy().astype(np.float64)
     assert np.abs(a - b).sum() / np.abs(b).sum() <= 1e-5
+
+
+@pytest.mark.parametrize("dist", ["normal", "uniform"])
+@pytest.mark.parametrize("n,d,sqrt_d", [(128, 128, False), (384, 128, True), (1024, 64, False),
+                                        (2048, 128, False)])
+def test_fast_mode_pp_kernel(ifa, oracle, dist, n, d, sqrt_d, monkeypatch):
+    """The two-Q-tile kernel (csrc/attn_pp.cu: fast, non-causal, Bc = 128,
+    n % 128 == 0; P.V as exact fp16 integers into an f32 TMEM accumulator)
+    meets the tolerance-mode bar against the oracle and agrees with the quad
+    kernel (IFA_B200_NO_PP=1) far inside it.  n = 384 has an odd number of
+    Q tiles (the second tile of the last pair is all padding)."""
+    _, (qc, qs, kc, ks, vc, vs) = _quantized_case(oracle, dist, n, d, seed=3 * n + d)
+    want = oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, 128,
+                                      flags=1 if sqrt_d else 0)
+    inputs = ifa.QuantizedAttentionInputs(
+        ifa.QuantizedRows(_dev(qc), _dev(qs)), ifa.QuantizedRows(_dev(kc), _dev(ks)),
+        ifa.QuantizedTensor(_dev(vc), _dev(np.asarray(vs, np.float32))))
+    cfg = ifa.AttentionConfig(ifa.BlockSpec(64, 128), apply_sqrt_d_scaling=sqrt_d, fast=True)
+    got = ifa.int_flash_attention(inputs, cfg).cpu().numpy()
+    mre, mx, bound = _fast_close(got, want, vc, vs)
+    assert mre <= FAST_MRE and mx <= bound, (mre, mx, bound)
+    monkeypatch.setenv("IFA_B200_NO_PP", "1")
+    quad = ifa.int_flash_attention(inputs, cfg).cpu().numpy().astype(np.float64)
+    assert np.abs(got - quad).sum() / np.abs(quad).sum() <= 1e-5
+
+
+def test_fast_mode_pp_batched_slices(ifa, oracle):
+    """Several (b,h) slices through the two-Q-tile kernel (the V tiles are
+    addressed across the flattened slice dimension)."""
+    b, h, n, d = 2, 3, 256, 128
+    rng = np.random.default_rng(5)
+    x = [rng.standard_normal((b, h, n, d)).astype(np.float32) for _ in range(3)]
+    qq = ifa.quantize_per_row(_dev(x[0]))
+    kq = ifa.quantize_per_row(_dev(x[1]))
+    vq = ifa.quantize_per_tensor(_dev(x[2]))
+    got = ifa.int_flash_attention(ifa.QuantizedAttentionInputs(qq, kq, vq),
+                                  ifa.AttentionConfig(ifa.BlockSpec(128, 128), fast=True))
+    got = got.cpu().numpy()
+    qc, qs = qq.values.cpu().numpy(), qq.scales.cpu().numpy()
+    kc, ks = kq.values.cpu().numpy(), kq.scales.cpu().numpy()
+    vc, vs = vq.values.cpu().numpy(), vq.scale.cpu().numpy()
+    for bi in range(b):
+        for hi in range(h):
+            want = oracle.int_flash_attention(qc[bi, hi], qs[bi, hi], kc[bi, hi], ks[bi, hi],
+                                              vc[bi, hi], float(vs[bi, hi]), 128, 128)
+            mre, mx, bound = _fast_close(got[bi, hi], want, vc[bi, hi], vs[bi, hi])
+            assert mre <= FAST_MRE and mx <= bound, (bi, hi, mre, mx)
