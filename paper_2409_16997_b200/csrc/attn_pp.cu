@@ -85,6 +85,7 @@ struct Params {
     float* o;
     int32_t n, d;
     float sk_mul;  // log2(e) [* 1/sqrt(d)]: scores are kept in the log2 domain
+    uint32_t flags;
     int32_t pairs, slices, items;
 };
 
@@ -100,6 +101,32 @@ struct Ring {
 };
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+// Work item -> (pair of Q tiles, slice, KV tiles the pair reads).  Causal:
+// the pairs nearest the diagonal end have the most keys and go first
+// (longest-processing-time order); group g of pair t sees KV tiles
+// 0 .. 2t + g and masks inside tile 2t + g.
+struct PWork {
+    int32_t pair, slice, jt;
+};
+__device__ __forceinline__ PWork pwork(int32_t idx, const Params& p, bool causal, int32_t J) {
+    PWork w;
+    if (causal) {
+        w.pair = p.pairs - 1 - idx / p.slices;
+        w.slice = idx % p.slices;
+        w.jt = 2 * w.pair + 2 < J ? 2 * w.pair + 2 : J;
+    } else {
+        w.pair = idx % p.pairs;
+        w.slice = idx / p.pairs;
+        w.jt = J;
+    }
+    return w;
+}
+__device__ __forceinline__ int32_t group_tiles(const PWork& w, int g, bool causal, int32_t J) {
+    if (!causal) return J;
+    const int32_t t = 2 * w.pair + g + 1;
+    return t < J ? t : J;
+}
 
 __device__ __forceinline__ float ex2(float t) {
     float r;
@@ -179,7 +206,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
     const int32_t n = p.n;
-    const int32_t J = n / BN;  // KV tiles per item (n % 128 == 0)
+    const int32_t J = n / BN;  // KV tiles of a slice (n % 128 == 0)
+    const bool causal = (p.flags & IFA_FLAG_CAUSAL) != 0;
 
     const uint32_t b_q_full = smem_u32(&sm.q_full), b_q_empty = smem_u32(&sm.q_empty);
     const uint32_t b_k_full = smem_u32(&sm.k_full[0]), b_k_empty = smem_u32(&sm.k_empty[0]);
@@ -231,7 +259,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             Ring<VST> vr;
             uint32_t i = 0, wi = 0;
             for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x, ++wi) {
-                const int32_t q0 = (idx % p.pairs) * 2 * BM, slice = idx / p.pairs;
+                const PWork w = pwork(idx, p, causal, J);
+                const int32_t q0 = w.pair * 2 * BM, slice = w.slice;
                 if (lane == 0) {
                     if (wi >= 1) bar_wait(b_q_empty, (wi - 1) & 1);
                     mbar_arrive_expect_tx(&sm.q_full, 2 * BM * D);
@@ -239,7 +268,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     tma_load_3d(sm.q[1], &tm_q, &sm.q_full, 0, q0 + BM, slice, pol_stream);
                 }
                 const float* sk_slice = p.sk + static_cast<int64_t>(slice) * n;
-                for (int32_t key0 = 0; key0 < n; key0 += BN) {
+                for (int32_t key0 = 0; key0 < w.jt * BN; key0 += BN) {
                     const uint32_t ks = kr.idx, vs = vr.idx;
                     if (i >= KST) bar_wait(b_k_empty + 8 * ks, kr.phase ^ 1u);
                     float4 k4 = __ldg(reinterpret_cast<const float4*>(sk_slice + key0) + lane);
@@ -298,16 +327,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const uint32_t p_base = smem_u32(sm.p[g]);
                 for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x, ++wi) {
                     const bool has_next_item = idx + static_cast<int32_t>(gridDim.x) < p.items;
-                    for (int32_t j = 0; j < J; ++j, ++t) {
-                        Ring<KST> nk = kr;
-                        nk.advance();
-                        const bool last = j == J - 1;
+                    const PWork w = pwork(idx, p, causal, J);
+                    const int32_t jg = group_tiles(w, g, causal, J);
+                    for (int32_t j = 0; j < w.jt; ++j) {
+                        if (j >= jg) {  // causal: a KV tile only the other group reads
+                            bar_wait(b_k_full + 8 * kr.idx, kr.phase);
+                            bar_arrive(b_k_empty + 8 * kr.idx);
+                            bar_wait(b_v_full + 8 * vr.idx, vr.phase);
+                            bar_arrive(b_v_empty + 8 * vr.idx);
+                            kr.advance();
+                            vr.advance();
+                            continue;
+                        }
+                        const bool last = j == jg - 1;
                         mma_commit_u32(b_k_empty + 8 * kr.idx);  // S(j) issued
                         if (last) {
                             mma_commit_u32(b_q_empty);  // every S of this item issued
                             if (has_next_item) bar_wait(b_q_full, (wi + 1) & 1);
                         }
                         if (!last || has_next_item) {
+                            // next S: tile j+1, or tile 0 of the next item (jt - j ring
+                            // positions ahead)
+                            Ring<KST> nk = kr;
+                            const int32_t ahead = last ? w.jt - j : 1;
+                            for (int32_t a = 0; a < ahead; ++a) nk.advance();
                             bar_wait(b_s_empty + 8 * g, t & 1);
                             issue_s(nk.idx, nk.phase);
                         }
@@ -330,6 +373,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         mma_commit_u32(b_v_empty + 8 * vr.idx);
                         kr.advance();
                         vr.advance();
+                        ++t;
                     }
                 }
             }
@@ -363,8 +407,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t tc = 0, wi = 0;
 
         for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x, ++wi) {
-            const int32_t q0 = (idx % p.pairs) * 2 * BM + static_cast<int32_t>(g) * BM;
-            const int32_t slice = idx / p.pairs;
+            const PWork w = pwork(idx, p, causal, J);
+            const int32_t jg = group_tiles(w, static_cast<int>(g), causal, J);
+            const int32_t diag = causal ? 2 * w.pair + static_cast<int32_t>(g) : -1;
+            const int32_t q0 = w.pair * 2 * BM + static_cast<int32_t>(g) * BM;
+            const int32_t slice = w.slice;
             int32_t grow[2];
             float sq[2];
 #pragma unroll
@@ -374,8 +421,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             float l[2] = {0.0f, 0.0f}, m[2] = {-__int_as_float(0x7f800000), -__int_as_float(0x7f800000)};
 
-            for (int32_t j = 0; j < J; ++j, ++tc) {
+            for (int32_t j = 0; j < w.jt; ++j) {
                 const uint32_t st = kv.idx;
+                if (j >= jg) {  // causal: the other group's diagonal tile
+                    bar_wait(b_k_full + 8 * st, kv.phase);
+                    __syncwarp();
+                    if (lane == 0) bar_arrive(b_k_empty + 8 * st);
+                    kv.advance();
+                    continue;
+                }
                 bar_wait(bs_full, tc & 1);
                 tc_fence_after();
                 uint32_t sr[64];
@@ -406,6 +460,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
                 __syncwarp();
                 if (lane == 0) bar_arrive(b_k_empty + 8 * st);
+                const bool dmask = j == diag;  // keys > row inside the diagonal tile
+                if (dmask) {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k)
+#pragma unroll
+                        for (int r = 0; r < 2; ++r)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e)
+                                if (8 * k + 2 * static_cast<int32_t>(t0) + e > row0 + 8 * r)
+                                    u[4 * k + 2 * r + e] = -__int_as_float(0x7f800000);
+                }
                 float cr[2], alpha[2];
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
@@ -440,7 +505,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                                f2(sq[r]), f2(cr[r]));
                         const float2 y = (k & kPolyMask) == kPolyMask ? exp2_poly2(t)
                                                       : make_float2(ex2(t.x), ex2(t.y));
-                        const float2 c = fsub2(fadd2(y, f2(kMagic)), f2(kMagic));
+                        float2 c = fsub2(fadd2(y, f2(kMagic)), f2(kMagic));
+                        if (dmask) {  // masked keys weigh 0 (also when sQ == 0)
+                            const int32_t key = 8 * k + 2 * static_cast<int32_t>(t0);
+                            if (key > row0 + 8 * r) c.x = 0.0f;
+                            if (key + 1 > row0 + 8 * r) c.y = 0.0f;
+                        }
                         ls[r] = fadd2(ls[r], c);
                         const __half2 h = __floats2half2_rn(c.x, c.y);
                         wd[r][k] = *reinterpret_cast<const uint32_t*>(&h);
@@ -488,6 +558,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int r = 0; r < 2; ++r) l[r] = __fmaf_rn(l[r], alpha[r], ls[r].x + ls[r].y);
                 kv.advance();
+                ++tc;
             }
             // epilogue: O * sV / l, l summed over the quad
             const float sv = p.sv[slice];
@@ -653,6 +724,7 @@ static cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     p.o = a.o;
     p.n = static_cast<int32_t>(a.n);
     p.d = static_cast<int32_t>(a.d);
+    p.flags = a.flags;
     p.sk_mul = kLog2e * ((a.flags & IFA_FLAG_SQRT_D) ? 1.0f / sqrtf(static_cast<float>(a.d)) : 1.0f);
     const int32_t q_tiles = static_cast<int32_t>((a.n + BM - 1) / BM);
     p.pairs = (q_tiles + 1) / 2;
@@ -691,7 +763,7 @@ bool int_flash_pp_eligible(const AttnArgs& a) {
     if (off && off[0] == '1') return false;
     const int64_t bc = a.bc < a.n ? a.bc : a.n;
     const bool tiles_are_blocks = bc == pp::BN || (bc == a.n && a.n <= pp::BN);
-    return (a.flags & IFA_FLAG_FAST) && !(a.flags & IFA_FLAG_CAUSAL) &&
+    return (a.flags & IFA_FLAG_FAST) &&
            a.audit == nullptr && tiles_are_blocks && a.n % 128 == 0 && a.d <= 128;
 }
 

@@ -265,9 +265,8 @@ def _fast_close(got, want, vc, vs):
 @pytest.mark.parametrize("dist", ["normal", "uniform"])
 @pytest.mark.parametrize("causal", [False, True])
 def test_fast_mode_within_tolerance(ifa, oracle, n, d, dist, causal):
-    """Non-causal n % 128 == 0 runs the two-Q-tile kernel (attn_pp.cu), other
-    n % 32 == 0 shapes the quad-layout kernel (8 math warps), the rest the
-    16-warp one."""
+    """n % 128 == 0 runs the two-Q-tile kernel (attn_pp.cu), other n % 32 == 0
+    shapes the quad-layout kernel (8 math warps), the rest the 16-warp one."""
     _, (qc, qs, kc, ks, vc, vs) = _quantized_case(oracle, dist, n, d, seed=n + d)
     want = oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, 128,
                                       flags=2 if causal else 0)
@@ -313,21 +312,25 @@ def test_fast_mode_both_kernels_agree(ifa, oracle, n, d, causal, monkeypatch):
 
 
 @pytest.mark.parametrize("dist", ["normal", "uniform"])
-@pytest.mark.parametrize("n,d,sqrt_d", [(128, 128, False), (384, 128, True), (1024, 64, False),
-                                        (2048, 128, False)])
-def test_fast_mode_pp_kernel(ifa, oracle, dist, n, d, sqrt_d, monkeypatch):
-    """The two-Q-tile kernel (csrc/attn_pp.cu: fast, non-causal, Bc = 128,
-    n % 128 == 0; P.V as exact fp16 integers into an f32 TMEM accumulator)
-    meets the tolerance-mode bar against the oracle and agrees with the quad
-    kernel (IFA_B200_NO_PP=1) far inside it.  n = 384 has an odd number of
-    Q tiles (the second tile of the last pair is all padding)."""
+@pytest.mark.parametrize("n,d,sqrt_d,causal", [(128, 128, False, False), (384, 128, True, False),
+                                               (1024, 64, False, False), (2048, 128, False, False),
+                                               (128, 64, False, True), (384, 128, False, True),
+                                               (1024, 128, True, True), (2048, 64, False, True)])
+def test_fast_mode_pp_kernel(ifa, oracle, dist, n, d, sqrt_d, causal, monkeypatch):
+    """The two-Q-tile kernel (csrc/attn_pp.cu: fast, Bc = 128, n % 128 == 0;
+    P.V as exact fp16 integers into an f32 TMEM accumulator) meets the
+    tolerance-mode bar against the oracle and agrees with the quad kernel
+    (IFA_B200_NO_PP=1) far inside it.  n = 384 has an odd number of Q tiles
+    (the second tile of the last pair is all padding); causal pairs give the
+    two groups different KV tile counts."""
     _, (qc, qs, kc, ks, vc, vs) = _quantized_case(oracle, dist, n, d, seed=3 * n + d)
     want = oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, 128,
-                                      flags=1 if sqrt_d else 0)
+                                      flags=(1 if sqrt_d else 0) | (2 if causal else 0))
     inputs = ifa.QuantizedAttentionInputs(
         ifa.QuantizedRows(_dev(qc), _dev(qs)), ifa.QuantizedRows(_dev(kc), _dev(ks)),
         ifa.QuantizedTensor(_dev(vc), _dev(np.asarray(vs, np.float32))))
-    cfg = ifa.AttentionConfig(ifa.BlockSpec(64, 128), apply_sqrt_d_scaling=sqrt_d, fast=True)
+    cfg = ifa.AttentionConfig(ifa.BlockSpec(64, 128), apply_sqrt_d_scaling=sqrt_d,
+                              causal=causal, fast=True)
     got = ifa.int_flash_attention(inputs, cfg).cpu().numpy()
     mre, mx, bound = _fast_close(got, want, vc, vs)
     assert mre <= FAST_MRE and mx <= bound, (mre, mx, bound)
