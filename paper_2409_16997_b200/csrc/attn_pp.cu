@@ -102,10 +102,12 @@ struct Ring {
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
-// Work item -> (pair of Q tiles, slice, KV tiles the pair reads).  Causal:
-// the pairs nearest the diagonal end have the most keys and go first
-// (longest-processing-time order); group g of pair t sees KV tiles
-// 0 .. 2t + g and masks inside tile 2t + g.
+// Work item -> (pair of Q tiles, slice, KV tiles the pair reads).
+// Non-causal: the pairs of one slice are adjacent, so CTAs running together
+// share the slice's K and V in L2.  Causal: the pairs nearest the diagonal
+// end have the most keys and go first (longest-processing-time order);
+// group g of pair t sees KV tiles 0 .. 2t + g and masks inside tile 2t + g.
+// (A slice-major causal order measured slower on C3: worse balance.)
 struct PWork {
     int32_t pair, slice, jt;
 };
@@ -763,6 +765,12 @@ bool int_flash_pp_eligible(const AttnArgs& a) {
     if (off && off[0] == '1') return false;
     const int64_t bc = a.bc < a.n ? a.bc : a.n;
     const bool tiles_are_blocks = bc == pp::BN || (bc == a.n && a.n <= pp::BN);
+    // causal: correct (tests), but on C3 the pair-ordered LPT schedule keeps
+    // all slices' K and fp16 V (192 MB) in flight and loses to the quad
+    // kernel (2.71 vs 2.55 ms), so it is opt-in
+    const char* pc = std::getenv("IFA_B200_PP_CAUSAL");
+    const bool causal_ok = pc && pc[0] == '1';
+    if ((a.flags & IFA_FLAG_CAUSAL) && !causal_ok) return false;
     return (a.flags & IFA_FLAG_FAST) &&
            a.audit == nullptr && tiles_are_blocks && a.n % 128 == 0 && a.d <= 128;
 }
