@@ -670,3 +670,159 @@ int ifa_or_code_bounds_exhaustive(float *out, int threads) {
     free(cs);
     return mono;
 }
+
+
+/* ------------------------------------------------------------------ fp8 (f3)
+ * fp8.cpp:17-24 round_ties_even on an exact double quotient. */
+static int64_t or_round_ties_even(double v) {
+    const double fl = floor(v);
+    const double diff = v - fl;
+    const int64_t n = (int64_t)fl;
+    if (diff > 0.5) return n + 1;
+    if (diff < 0.5) return n;
+    return (n % 2 == 0) ? n : n + 1;
+}
+
+/* fp8.cpp:28-57 */
+uint8_t ifa_or_e4m3_encode(float x) {
+    const uint8_t sign = signbit(x) ? 0x80 : 0x00;
+    if (isnan(x)) return sign | 0x7f;
+    const double a = fabs((double)x);
+    if (a == 0.0) return sign;
+    if (a > 448.0) return sign | 0x7e;
+    int e = ilogb(a);
+    if (e < -6) e = -6;
+    int64_t q = or_round_ties_even(ldexp(a, -(e - 3)));
+    if (e == -6 && q < 8) return sign | (uint8_t)q;
+    if (q == 16) {
+        e += 1;
+        q = 8;
+    }
+    return sign | (uint8_t)((uint8_t)(e + 7) << 3) | (uint8_t)(q - 8);
+}
+
+/* fp8.cpp:59-72 */
+float ifa_or_e4m3_decode(uint8_t bits) {
+    const int exp_field = (bits >> 3) & 0xf;
+    const int mant = bits & 0x7;
+    if (exp_field == 0xf && mant == 0x7) return NAN;
+    double v;
+    if (exp_field == 0)
+        v = ldexp((double)mant / 8.0, -6);
+    else
+        v = ldexp(1.0 + (double)mant / 8.0, exp_field - 7);
+    return (float)((bits & 0x80) ? -v : v);
+}
+
+/* fp8.cpp:78-97 */
+int ifa_or_fp8_roundtrip(const float *x, int64_t count, float *out, uint8_t *codes, float *scale) {
+    float max_abs = 0.0f;
+    for (int64_t i = 0; i < count; ++i) {
+        if (!isfinite(x[i])) return -1;
+        const float a = fabsf(x[i]);
+        max_abs = max_abs < a ? a : max_abs;
+    }
+    if (max_abs == 0.0f) {
+        for (int64_t i = 0; i < count; ++i) {
+            out[i] = 0.0f;
+            if (codes) codes[i] = 0;
+        }
+        if (scale) *scale = 0.0f;
+        return 0;
+    }
+    const float s = 448.0f / max_abs;
+    for (int64_t i = 0; i < count; ++i) {
+        const uint8_t c = ifa_or_e4m3_encode(x[i] * s);
+        out[i] = ifa_or_e4m3_decode(c) / s;
+        if (codes) codes[i] = c;
+    }
+    if (scale) *scale = s;
+    return 0;
+}
+
+/* attention.cpp:401-407 -> flash_attention_float (:194-211) over the
+ * roundtripped matrices; tiled_float_attention / merge_softmax_state /
+ * finalize_softmax_state as in ifa_or_half_int8_attention above. */
+int ifa_or_fp8_attention(const float *q, const float *k, const float *v, int64_t n, int64_t d,
+                         int64_t br_cfg, int64_t bc_cfg, uint32_t flags, float *out) {
+    if (n < 1 || d < 1) return -1;
+    if (br_cfg < 1 || bc_cfg < 1) return -1;
+    const int64_t cnt = n * d;
+    float *qr = (float *)malloc(sizeof(float) * cnt);
+    float *kr = (float *)malloc(sizeof(float) * cnt);
+    float *vr = (float *)malloc(sizeof(float) * cnt);
+    if (!qr || !kr || !vr) return -3;
+    if (ifa_or_fp8_roundtrip(q, cnt, qr, NULL, NULL) || ifa_or_fp8_roundtrip(k, cnt, kr, NULL, NULL) ||
+        ifa_or_fp8_roundtrip(v, cnt, vr, NULL, NULL)) {
+        free(qr);
+        free(kr);
+        free(vr);
+        return -1;
+    }
+    const float extra = (flags & IFA_OR_FLAG_SQRT_D) ? 1.0f / sqrtf((float)d) : 1.0f;
+    const int64_t br_max = br_cfg < n ? br_cfg : n;
+    const int64_t bc_max = bc_cfg < n ? bc_cfg : n;
+    float *s = (float *)malloc(sizeof(float) * br_max * bc_max);
+    float *p = (float *)malloc(sizeof(float) * br_max * bc_max);
+    float *acc = (float *)malloc(sizeof(float) * br_max * d);
+    float *m = (float *)malloc(sizeof(float) * br_max);
+    float *l = (float *)malloc(sizeof(float) * br_max);
+    if (!s || !p || !acc || !m || !l) return -3;
+    for (int64_t i0 = 0; i0 < n; i0 += br_cfg) {
+        const int64_t br = (br_cfg < n - i0) ? br_cfg : n - i0;
+        for (int64_t r = 0; r < br; ++r) {
+            m[r] = -INFINITY;
+            l[r] = 0.0f;
+        }
+        memset(acc, 0, sizeof(float) * br * d);
+        for (int64_t j0 = 0; j0 < n; j0 += bc_cfg) {
+            const int64_t bc = (bc_cfg < n - j0) ? bc_cfg : n - j0;
+            /* fill (:200-210): float_gemm_nt_strided (gemm.cpp:65-78) [*= extra] */
+            for (int64_t r = 0; r < br; ++r)
+                for (int64_t c = 0; c < bc; ++c) {
+                    const float *a = qr + (i0 + r) * d;
+                    const float *b = kr + (j0 + c) * d;
+                    float accd = 0.0f;
+                    for (int64_t t = 0; t < d; ++t) accd += a[t] * b[t];
+                    s[r * bc + c] = accd;
+                }
+            if (extra != 1.0f)
+                for (int64_t idx = 0; idx < br * bc; ++idx) s[idx] *= extra;
+            for (int64_t r = 0; r < br; ++r) {
+                float m_loc = -INFINITY;
+                for (int64_t c = 0; c < bc; ++c)
+                    m_loc = (m_loc < s[r * bc + c]) ? s[r * bc + c] : m_loc;
+                const float m_new = (m[r] < m_loc) ? m_loc : m[r];
+                const float alpha = ifa_or_expf(m[r] - m_new);
+                float row_sum = 0.0f;
+                for (int64_t c = 0; c < bc; ++c) {
+                    const float e = ifa_or_expf(s[r * bc + c] - m_new);
+                    p[r * bc + c] = e;
+                    row_sum += e;
+                }
+                l[r] = l[r] * alpha + row_sum;
+                for (int64_t c = 0; c < d; ++c) acc[r * d + c] *= alpha;
+                m[r] = m_new;
+            }
+            for (int64_t r = 0; r < br; ++r)
+                for (int64_t t = 0; t < bc; ++t) {
+                    const float av = p[r * bc + t];
+                    const float *bt = vr + (j0 + t) * d;
+                    for (int64_t c = 0; c < d; ++c) acc[r * d + c] += av * bt[c];
+                }
+        }
+        for (int64_t r = 0; r < br; ++r) {
+            const float inv = 1.0f / l[r];
+            for (int64_t c = 0; c < d; ++c) out[(i0 + r) * d + c] = acc[r * d + c] * inv;
+        }
+    }
+    free(s);
+    free(p);
+    free(acc);
+    free(m);
+    free(l);
+    free(qr);
+    free(kr);
+    free(vr);
+    return 0;
+}

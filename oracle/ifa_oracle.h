@@ -81,6 +81,18 @@ int ifa_or_untiled_int8_attention(const int8_t *q, const float *sq, const int8_t
 int ifa_or_half_int8_attention(const int8_t *q, const float *sq, const int8_t *k,
                                const float *sk, const float *v, int64_t n, int64_t d,
                                int64_t br, int64_t bc, uint32_t flags, float *out);
+/* fp8.cpp:17-97: e4m3 encode (round half to even on the exact double
+ * quotient, saturate at 448, subnormal step 2^-9), decode, and the
+ * per-matrix roundtrip (s = 448 / max|x|; x -> decode(encode(x*s)) / s).
+ * ifa_or_fp8_roundtrip returns -1 on non-finite input (fp8.cpp:82-84);
+ * codes / scale (optional) receive the e4m3 bytes and s (0 for all-zero). */
+uint8_t ifa_or_e4m3_encode(float x);
+float ifa_or_e4m3_decode(uint8_t bits);
+int ifa_or_fp8_roundtrip(const float *x, int64_t count, float *out, uint8_t *codes, float *scale);
+/* attention.cpp:401-407 fp8_emulated_attention = flash_attention_float
+ * (:194-211, tiled_float_attention :49-80) over the three roundtrips. */
+int ifa_or_fp8_attention(const float *q, const float *k, const float *v, int64_t n, int64_t d,
+                         int64_t br, int64_t bc, uint32_t flags, float *out);
 int ifa_or_reference_attention(const float *q, const float *k, const float *v, int64_t n,
                                int64_t m, int64_t d, int64_t dv, uint32_t flags, float *out);
 

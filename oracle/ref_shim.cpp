@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "ifa/attention.hpp"
+#include "ifa/fp8.hpp"
 #include "ifa/gemm.hpp"
 #include "ifa/generate.hpp"
 #include "ifa/oracles.hpp"
@@ -237,6 +238,33 @@ int ifa_ref_half_int8_attention(const int8_t* q, const float* sq, const int8_t* 
         cfg.blocks = ifa::BlockSpec{br, bc};
         cfg.apply_sqrt_d_scaling = sqrt_d != 0;
         const ifa::FloatMatrix o = ifa::half_int8_attention(qr, kr, to_fm(v, n, d), cfg);
+        std::memcpy(out, o.data(), sizeof(float) * static_cast<size_t>(n * d));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int ifa_ref_fp8_roundtrip(const float* x, int64_t rows, int64_t cols, float* out) {
+    try {
+        const ifa::FloatMatrix o = ifa::fp8_e4m3_roundtrip(to_fm(x, rows, cols));
+        std::memcpy(out, o.data(), sizeof(float) * static_cast<size_t>(rows * cols));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+uint8_t ifa_ref_e4m3_encode(float x) { return ifa::e4m3_encode(x); }
+
+int ifa_ref_fp8_attention(const float* q, const float* k, const float* v, int64_t n, int64_t d,
+                          int64_t br, int64_t bc, int sqrt_d, float* out) {
+    try {
+        ifa::AttentionConfig cfg;
+        cfg.blocks = ifa::BlockSpec{br, bc};
+        cfg.apply_sqrt_d_scaling = sqrt_d != 0;
+        const ifa::FloatMatrix o =
+            ifa::fp8_emulated_attention(to_fm(q, n, d), to_fm(k, n, d), to_fm(v, n, d), cfg);
         std::memcpy(out, o.data(), sizeof(float) * static_cast<size_t>(n * d));
         return 0;
     } catch (const std::exception& e) {

@@ -79,6 +79,14 @@ class Oracle:
         L.ifa_or_half_int8_attention.argtypes = [_i8p, _f32p, _i8p, _f32p, _f32p, C.c_int64,
                                                  C.c_int64, C.c_int64, C.c_int64, C.c_uint32,
                                                  _f32p]
+        L.ifa_or_e4m3_encode.restype = C.c_uint8
+        L.ifa_or_e4m3_encode.argtypes = [C.c_float]
+        L.ifa_or_e4m3_decode.restype = C.c_float
+        L.ifa_or_e4m3_decode.argtypes = [C.c_uint8]
+        L.ifa_or_fp8_roundtrip.argtypes = [_f32p, C.c_int64, _f32p, C.c_void_p,
+                                           C.POINTER(C.c_float)]
+        L.ifa_or_fp8_attention.argtypes = [_f32p, _f32p, _f32p, C.c_int64, C.c_int64, C.c_int64,
+                                           C.c_int64, C.c_uint32, _f32p]
         L.ifa_or_error_accum.argtypes = [_f32p, _f32p, C.c_int64, C.POINTER(C.c_double),
                                          C.POINTER(C.c_double)]
         L.ifa_or_fnv1a64.restype = C.c_uint64
@@ -179,6 +187,30 @@ class Oracle:
             raise ValueError("half_int8_attention: invalid argument")
         return out
 
+    def e4m3_encode(self, x):
+        return self.lib.ifa_or_e4m3_encode(float(x))
+
+    def e4m3_decode(self, b):
+        return self.lib.ifa_or_e4m3_decode(int(b))
+
+    def fp8_roundtrip(self, x):
+        """fp8.cpp:78-97 over the whole array: (restored, e4m3 codes, scale s)."""
+        x = _f32(x)
+        out = np.empty(x.shape, np.float32)
+        codes = np.empty(x.shape, np.uint8)
+        sc = C.c_float(0.0)
+        if self.lib.ifa_or_fp8_roundtrip(x, x.size, out, codes.ctypes.data, C.byref(sc)):
+            raise ValueError("fp8_e4m3_roundtrip: non-finite input")
+        return out, codes, sc.value
+
+    def fp8_attention(self, q, k, v, br=64, bc=64, flags=0):
+        q, k, v = _f32(q), _f32(k), _f32(v)
+        n, d = q.shape
+        out = np.empty((n, d), np.float32)
+        if self.lib.ifa_or_fp8_attention(q, k, v, n, d, br, bc, flags, out):
+            raise ValueError("fp8_emulated_attention: invalid argument")
+        return out
+
     def reference_attention(self, q, k, v, flags=0):
         q, k, v = _f32(q), _f32(k), _f32(v)
         out = np.empty((q.shape[0], v.shape[1]), np.float32)
@@ -230,6 +262,11 @@ class Reference:
         L.ifa_ref_half_int8_attention.argtypes = [_i8p, _f32p, _i8p, _f32p, _f32p, C.c_int64,
                                                   C.c_int64, C.c_int64, C.c_int64, C.c_int,
                                                   _f32p]
+        L.ifa_ref_fp8_roundtrip.argtypes = [_f32p, C.c_int64, C.c_int64, _f32p]
+        L.ifa_ref_e4m3_encode.restype = C.c_uint8
+        L.ifa_ref_e4m3_encode.argtypes = [C.c_float]
+        L.ifa_ref_fp8_attention.argtypes = [_f32p, _f32p, _f32p, C.c_int64, C.c_int64,
+                                            C.c_int64, C.c_int64, C.c_int, _f32p]
         L.ifa_ref_expf.restype = C.c_float
         L.ifa_ref_expf.argtypes = [C.c_float]
 
@@ -309,6 +346,22 @@ class Reference:
 
     def expf(self, x):
         return self.lib.ifa_ref_expf(float(x))
+
+    def e4m3_encode(self, x):
+        return self.lib.ifa_ref_e4m3_encode(float(x))
+
+    def fp8_roundtrip(self, x):
+        x = _f32(x)
+        out = np.empty(x.shape, np.float32)
+        self._check(self.lib.ifa_ref_fp8_roundtrip(x, x.shape[0], x.shape[1], out))
+        return out
+
+    def fp8_attention(self, q, k, v, br=64, bc=64, sqrt_d=False):
+        q, k, v = _f32(q), _f32(k), _f32(v)
+        n, d = q.shape
+        out = np.empty((n, d), np.float32)
+        self._check(self.lib.ifa_ref_fp8_attention(q, k, v, n, d, br, bc, int(sqrt_d), out))
+        return out
 
     def half_int8_attention(self, q, sq, k, sk, v, br=64, bc=64, sqrt_d=False):
         q, k = _i8(q), _i8(k)
