@@ -182,6 +182,49 @@ def half_int8_timing(torch, plan, v, slices, n, d, ops, stream, steps) -> dict:
     return res
 
 
+def fp8_timing(torch, q, k, v, slices, n, d, ops, stream, steps) -> dict:
+    """SURVEY §8(f) f3 on the same f32 inputs: fp8_e4m3_roundtrip of Q, K, V
+    (per slice, e4m3 codes + decoded V) and the FP8 forward (S on tcgen05
+    kind::f8f6f4), timed separately."""
+    from paper_2409_16997_b200 import _lib
+    lib = _lib.load()
+    dev = q.device
+    codes = [torch.empty(q.shape, dtype=torch.uint8, device=dev) for _ in range(3)]
+    scales = [torch.empty((slices,), dtype=torch.float32, device=dev) for _ in range(3)]
+    dec = torch.empty(q.shape, dtype=torch.float16, device=dev)
+    ws = torch.empty((slices,), dtype=torch.int32, device=dev)
+    out = torch.empty(q.shape, dtype=torch.float32, device=dev)
+    sp = stream.cuda_stream
+
+    def quant():
+        for i, t in enumerate((q, k, v)):
+            _lib.check(lib.ifa_fp8_quantize_per_tensor(
+                t.data_ptr(), slices, n, d, codes[i].data_ptr(),
+                dec.data_ptr() if i == 2 else None, scales[i].data_ptr(), ws.data_ptr(), None,
+                sp))
+
+    def fwd():
+        _lib.check(lib.ifa_fp8_attention_fwd(codes[0].data_ptr(), scales[0].data_ptr(),
+                                             codes[1].data_ptr(), scales[1].data_ptr(),
+                                             dec.data_ptr(), scales[2].data_ptr(),
+                                             out.data_ptr(), slices, n, d, 128, 128, 0, sp))
+
+    res = {}
+    for name, fn in (("quantize_ms", quant), ("attention_ms", fwd)):
+        for _ in range(2):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        res[name] = e0.elapsed_time(e1) / steps
+    res["attention_tops"] = ops / (res["attention_ms"] / 1e3) / 1e12
+    res["kernel"] = "half_int8_fwd_kernel<D, FP8> (e4m3 S on kind::f8f6f4, fp16 P.V)"
+    return res
+
+
 def fp16_sdpa_baseline(torch, dev, slices, n, d, causal, steps=5) -> dict:
     """FlashAttention FP16/BF16 on the same GPU and shape (torch SDPA)."""
     import torch.nn.functional as F
@@ -548,6 +591,11 @@ def main() -> None:
                                                      stream, max(3, args.steps // 2))
             except Exception as e:  # pragma: no cover
                 line["half_int8"] = {"error": str(e)[:200]}
+            try:
+                line["fp8"] = fp8_timing(torch, q, k, v, slices, N, d, ops_rank, stream,
+                                         max(3, args.steps // 2))
+            except Exception as e:  # pragma: no cover
+                line["fp8"] = {"error": str(e)[:200]}
         try:
             line["fp16_flash_baseline"] = fp16_sdpa_baseline(torch, dev, slices, N, d, causal)
         except Exception as e:  # pragma: no cover

@@ -121,6 +121,25 @@ int ifa_half_int8_fwd(const int8_t* q, const float* sq, const int8_t* k, const f
 /* DEVICE x[count] f32 -> out[count] fp16 (round to nearest even). */
 int ifa_convert_f16(const float* x, int64_t count, uint16_t* out, void* stream);
 
+/* ---- FP8 e4m3 baseline --------------------------------
+ * ifa_fp8_quantize_per_tensor  replaces fp8_e4m3_roundtrip (fp8.cpp:78-97)
+ *   per [rows x cols] slice: s = 448 / max|x|, codes = e4m3(x * s) (bitwise
+ *   the reference's e4m3_encode), slice_scales[s] = s (0 for an all-zero
+ *   slice); decoded_f16 (optional) receives decode(code) as fp16 (exact).
+ *   workspace: DEVICE uint32[slices].  Non-finite input: *nonfinite_index.
+ * ifa_fp8_attention_fwd  replaces fp8_emulated_attention
+ *   (attention.cpp:401-407): S = Q8.K8^T on tcgen05.mma kind::f8f6f4, s =
+ *   S / (sQ sK) [* 1/sqrt(d)], float online softmax, P (fp16) . V (decoded
+ *   e4m3 as fp16), O / (l * sV).  Tolerance semantics as the half-INT8 path
+ *   (tests/test_gpu_fp8.py).  d in {64, 128}; flags: SQRT_D only. */
+int ifa_fp8_quantize_per_tensor(const float* x, int64_t slices, int64_t rows, int64_t cols,
+                                uint8_t* codes, uint16_t* decoded_f16, float* slice_scales,
+                                void* workspace, int64_t* nonfinite_index, void* stream);
+int ifa_fp8_attention_fwd(const uint8_t* q, const float* q_scales, const uint8_t* k,
+                          const float* k_scales, const uint16_t* v_f16, const float* v_scales,
+                          float* o, int64_t slices, int64_t n, int64_t d, int64_t br, int64_t bc,
+                          uint32_t flags, void* stream);
+
 /* ---- host-buffer forms (drop-in for synchronous CPU callers) -------------
  * Same arguments as above, but every array is HOST memory (pageable or
  * pinned) and the call returns after the results are back on the host.

@@ -12,6 +12,9 @@ from .api import (  # noqa: F401
     QuantizedAttentionInputs,
     QuantizedRows,
     QuantizedTensor,
+    Fp8Tensor,
+    fp8_emulated_attention,
+    fp8_quantize_per_tensor,
     half_int8_attention,
     int_flash_attention,
     quantize_per_row,
@@ -22,6 +25,7 @@ from ._lib import NativeLibraryError  # noqa: F401
 
 __all__ = [
     "AttentionConfig", "BlockSpec", "PCodeAudit", "QuantizedAttentionInputs",
-    "QuantizedRows", "QuantizedTensor", "half_int8_attention", "int_flash_attention", "quantize_per_row",
+    "QuantizedRows", "QuantizedTensor", "Fp8Tensor", "fp8_emulated_attention",
+    "fp8_quantize_per_tensor", "half_int8_attention", "int_flash_attention", "quantize_per_row",
     "quantize_per_tensor", "version", "NativeLibraryError",
 ]

@@ -18,6 +18,8 @@ reference                      here
 ``PCodeAudit``                 :class:`PCodeAudit` (attention.hpp:75-80)
 ``int_flash_attention``        :func:`int_flash_attention` (attention.hpp:85-87)
 ``half_int8_attention``        :func:`half_int8_attention` (attention.hpp:93-96)
+``fp8_e4m3_roundtrip``         :func:`fp8_quantize_per_tensor` (fp8.hpp:24-27)
+``fp8_emulated_attention``     :func:`fp8_emulated_attention` (attention.hpp:98-101)
 =============================  ==============================================
 
 Tensors are ``torch`` CUDA tensors (PyTorch is only the device-memory and
@@ -286,6 +288,77 @@ def half_int8_attention(q: QuantizedRows, k: QuantizedRows, v: torch.Tensor,
                                      vh.data_ptr(), out.data_ptr(), slices, n, d,
                                      cfg.blocks.Br, cfg.blocks.Bc,
                                      _lib.FLAG_SQRT_D if cfg.apply_sqrt_d_scaling else 0, sp))
+    return out
+
+
+@dataclass
+class Fp8Tensor:
+    """e4m3 codes of a fp8_e4m3_roundtrip per (b,h) slice (fp8.cpp:78-97):
+    restored = decode(codes) / scale."""
+    codes: torch.Tensor     # uint8 [..., n, d] (e4m3 bit patterns)
+    scale: torch.Tensor     # f32 [...] (448 / max|x| per slice; 0 for all-zero)
+    decoded: torch.Tensor   # fp16 [..., n, d] = decode(codes), exact
+
+
+def fp8_quantize_per_tensor(x: torch.Tensor, *, check_finite: bool = True,
+                            stream: Optional[torch.cuda.Stream] = None) -> Fp8Tensor:
+    """fp8_e4m3_roundtrip's quantization of each trailing [rows, cols] matrix
+    on the GPU; codes bitwise equal to the reference's e4m3_encode."""
+    _require_cuda(x, torch.float32, "fp8_e4m3_roundtrip")
+    if x.dim() < 2:
+        raise ValueError("fp8_e4m3_roundtrip: expected a matrix [..., rows, cols]")
+    x = x.contiguous()
+    rows, cols = x.shape[-2], x.shape[-1]
+    slices = math.prod(x.shape[:-2]) if x.dim() > 2 else 1
+    codes = torch.empty(x.shape, dtype=torch.uint8, device=x.device)
+    dec = torch.empty(x.shape, dtype=torch.float16, device=x.device)
+    scale = torch.empty(x.shape[:-2], dtype=torch.float32, device=x.device)
+    ws = torch.empty(max(slices, 1), dtype=torch.int32, device=x.device)
+    bad = torch.full((1,), _INT64_MAX, dtype=torch.int64, device=x.device) if check_finite \
+        else None
+    lib = _lib.load()
+    _lib.check(lib.ifa_fp8_quantize_per_tensor(x.data_ptr(), slices, rows, cols,
+                                               codes.data_ptr(), dec.data_ptr(), scale.data_ptr(),
+                                               ws.data_ptr(),
+                                               bad.data_ptr() if bad is not None else None,
+                                               _stream_ptr(stream)))
+    if bad is not None and int(bad.item()) != _INT64_MAX:
+        raise ValueError("fp8_e4m3_roundtrip: non-finite input")  # fp8.cpp:82-84
+    return Fp8Tensor(codes, scale, dec)
+
+
+def fp8_emulated_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                           cfg: Optional[AttentionConfig] = None, *,
+                           out: Optional[torch.Tensor] = None,
+                           stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """fp8_emulated_attention (attention.cpp:401-407) on the GPU, natively in
+    FP8: e4m3 Q/K on the tensor core (tcgen05 kind::f8f6f4), float softmax,
+    P (fp16) . V (decoded e4m3).  f32 [..., n, d] in, f32 O out; within the
+    tolerance tests/test_gpu_fp8.py states of the reference."""
+    cfg = cfg or AttentionConfig()
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        _require_cuda(t, torch.float32, f"fp8_emulated_attention: {name}")
+    if q.dim() < 2 or q.shape[-2] < 1 or q.shape[-1] < 1:
+        raise ValueError("fp8_emulated_attention: empty input")
+    if tuple(k.shape) != tuple(q.shape) or tuple(v.shape) != tuple(q.shape):
+        raise NotImplementedError(
+            "fp8_emulated_attention: the sm_100a kernel takes q, k, v of one shape [..., n, d]")
+    cfg.validate()
+    if cfg.causal or cfg.fast:
+        raise NotImplementedError("fp8_emulated_attention: causal/fast are not part of this path")
+    n, d = q.shape[-2], q.shape[-1]
+    slices = q.numel() // (n * d)
+    q8, k8, v8 = (fp8_quantize_per_tensor(t, stream=stream) for t in (q, k, v))
+    if out is None:
+        out = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+    lib = _lib.load()
+    _lib.check(lib.ifa_fp8_attention_fwd(q8.codes.data_ptr(), q8.scale.data_ptr(),
+                                         k8.codes.data_ptr(), k8.scale.data_ptr(),
+                                         v8.decoded.data_ptr(), v8.scale.data_ptr(),
+                                         out.data_ptr(), slices, n, d, cfg.blocks.Br,
+                                         cfg.blocks.Bc,
+                                         _lib.FLAG_SQRT_D if cfg.apply_sqrt_d_scaling else 0,
+                                         _stream_ptr(stream)))
     return out
 
 

@@ -212,6 +212,58 @@ int ifa_half_int8_fwd(const int8_t* q, const float* sq, const int8_t* k, const f
     return e == cudaSuccess ? IFA_OK : cuda_fail(e, "half_int8_attention");
 }
 
+int ifa_fp8_quantize_per_tensor(const float* x, int64_t slices, int64_t rows, int64_t cols,
+                                uint8_t* codes, uint16_t* decoded_f16, float* slice_scales,
+                                void* workspace, int64_t* nonfinite_index, void* stream) {
+    g_err.clear();
+    if (slices < 0 || rows < 0 || cols < 0)
+        return fail(IFA_EINVAL, "fp8_e4m3_roundtrip: negative matrix extent");
+    if (slices == 0) return IFA_OK;
+    if (!slice_scales || !workspace) return fail(IFA_EINVAL, "fp8_e4m3_roundtrip: null pointer");
+    if (rows == 0 || cols == 0) {
+        const cudaError_t e = cudaMemsetAsync(slice_scales, 0, sizeof(float) * slices,
+                                              static_cast<cudaStream_t>(stream));
+        return e == cudaSuccess ? IFA_OK : cuda_fail(e, "fp8_e4m3_roundtrip");
+    }
+    if (!x || !codes) return fail(IFA_EINVAL, "fp8_e4m3_roundtrip: null pointer");
+    if ((rows * cols) % 2 != 0)
+        return fail(IFA_ENOTSUP, "fp8_e4m3_roundtrip: odd slice element count");
+    const cudaError_t e = ifa_b200::launch_fp8_quantize_per_tensor(
+        x, slices, rows, cols, codes, decoded_f16, slice_scales,
+        static_cast<uint32_t*>(workspace), nonfinite_index, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? IFA_OK : cuda_fail(e, "fp8_e4m3_roundtrip");
+}
+
+int ifa_fp8_attention_fwd(const uint8_t* q, const float* q_scales, const uint8_t* k,
+                          const float* k_scales, const uint16_t* v_f16, const float* v_scales,
+                          float* o, int64_t slices, int64_t n, int64_t d, int64_t br, int64_t bc,
+                          uint32_t flags, void* stream) {
+    g_err.clear();
+    if (slices < 0) return fail(IFA_EINVAL, "fp8_emulated_attention: negative slice count");
+    if (n < 1 || d < 1) return fail(IFA_EINVAL, "fp8_emulated_attention: empty input");
+    if (br < 1 || bc < 1) return fail(IFA_EINVAL, "BlockSpec: Br and Bc must be >= 1");
+    if (flags & ~IFA_FLAG_SQRT_D) {
+        if (flags & ~(IFA_FLAG_SQRT_D | IFA_FLAG_CAUSAL | IFA_FLAG_FAST))
+            return fail(IFA_EINVAL, "fp8_emulated_attention: unknown flag bits");
+        return fail(IFA_ENOTSUP, "fp8_emulated_attention: only IFA_FLAG_SQRT_D is supported");
+    }
+    if (d != 64 && d != 128)
+        return fail(IFA_ENOTSUP, "fp8_emulated_attention: head dim " + std::to_string(d) +
+                                     " not supported by the sm_100a kernel (64 or 128)");
+    if (slices == 0) return IFA_OK;
+    if (((n + 127) / 128) * slices > INT32_MAX)
+        return fail(IFA_ENOTSUP, "fp8_emulated_attention: too many work items");
+    if (!q || !q_scales || !k || !k_scales || !v_f16 || !v_scales || !o)
+        return fail(IFA_EINVAL, "fp8_emulated_attention: null pointer");
+    if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) |
+         reinterpret_cast<uintptr_t>(v_f16)) % 16 != 0)
+        return fail(IFA_EINVAL, "fp8_emulated_attention: q/k/v must be 16-byte aligned");
+    const cudaError_t e = ifa_b200::launch_fp8_attention_fwd(
+        q, q_scales, k, k_scales, v_f16, v_scales, o, slices, n, d,
+        (flags & IFA_FLAG_SQRT_D) != 0, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? IFA_OK : cuda_fail(e, "fp8_emulated_attention");
+}
+
 int ifa_convert_f16(const float* x, int64_t count, uint16_t* out, void* stream) {
     g_err.clear();
     if (count < 0) return fail(IFA_EINVAL, "convert_f16: negative count");

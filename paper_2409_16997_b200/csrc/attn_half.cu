@@ -67,8 +67,9 @@ struct alignas(1024) Smem {
 };
 
 struct Params {
-    const float* sq;
-    const float* sk;
+    const float* sq;  // half-INT8: per row [slices][n]; FP8: per slice [slices]
+    const float* sk;  // likewise
+    const float* sv;  // FP8: V roundtrip scale per slice (O /= sV); half-INT8: unused
     float* o;
     int32_t n, d;
     float sk_mul;  // log2(e) [* 1/sqrt(d)]: K scales staged pre-multiplied
@@ -125,12 +126,27 @@ __device__ __forceinline__ float ex2(float t) {
     return r;
 }
 
+__device__ __forceinline__ void mma_f8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
     const __half2 h = __floats2half2_rn(lo, hi);
     return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-template <int D>
+// FP8 = false: half-INT8 (int8 Q/K codes, per-row scales, S via kind::i8).
+// FP8 = true : SURVEY §8(f) f3, fp8_emulated_attention (attention.cpp:401-
+// 407): e4m3 Q/K codes with one scale per slice (fp8.cpp:78-97), S via
+// tcgen05.mma kind::f8f6f4 (f32 accumulate), V = the decoded e4m3 values as
+// fp16 (exact), O divided by the V scale at the end.
+template <int D, bool FP8>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     half_int8_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_k,
@@ -139,7 +155,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     constexpr uint32_t kSbo = 8 * D;
     constexpr uint32_t kKBytes = BN * D;
     constexpr uint32_t kVBytes = BN * D * 2;
-    constexpr uint32_t kIdescS = idesc_i8(BM, BN, false, false);
+    // kind::f8f6f4: D = F32 (bit 4), A = B = E4M3 (format fields 0)
+    constexpr uint32_t kIdescS =
+        FP8 ? ((1u << 4) | ((BN >> 3) << 17) | ((BM >> 4) << 24)) : idesc_i8(BM, BN, false, false);
     constexpr uint32_t kIdescPV = idesc_f16(BM, D, true);
     constexpr uint32_t kIdescSum = idesc_f16(BM, 16, false);
     const float kNegInf = -__int_as_float(0x7f800000);
@@ -201,15 +219,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     tma_load_3d(sm.q[qb], &tm_q, &sm.q_full[qb], 0, q0, slice, pol_stream);
                 }
                 const float* sk_slice = p.sk + static_cast<int64_t>(slice) * n;
+                // FP8: s = S / (sQ sK) for every key of the slice
+                const float c8 = FP8 ? __fdiv_rn(p.sk_mul, __fmul_rn(p.sq[slice], p.sk[slice])) : 0.0f;
                 for (int32_t key0 = 0; key0 < n; key0 += BN) {
                     const uint32_t st = kv.idx;
                     if (i >= STAGES) bar_wait(b_kv_empty + 8 * st, kv.phase ^ 1u);
                     float4 kv4;
                     const int32_t key = key0 + lane * 4;
-                    kv4.x = key + 0 < n ? sk_slice[key + 0] * p.sk_mul : 0.0f;
-                    kv4.y = key + 1 < n ? sk_slice[key + 1] * p.sk_mul : 0.0f;
-                    kv4.z = key + 2 < n ? sk_slice[key + 2] * p.sk_mul : 0.0f;
-                    kv4.w = key + 3 < n ? sk_slice[key + 3] * p.sk_mul : 0.0f;
+                    if constexpr (FP8) {
+                        kv4.x = key + 0 < n ? c8 : 0.0f;
+                        kv4.y = key + 1 < n ? c8 : 0.0f;
+                        kv4.z = key + 2 < n ? c8 : 0.0f;
+                        kv4.w = key + 3 < n ? c8 : 0.0f;
+                    } else {
+                        kv4.x = key + 0 < n ? sk_slice[key + 0] * p.sk_mul : 0.0f;
+                        kv4.y = key + 1 < n ? sk_slice[key + 1] * p.sk_mul : 0.0f;
+                        kv4.z = key + 2 < n ? sk_slice[key + 2] * p.sk_mul : 0.0f;
+                        kv4.w = key + 3 < n ? sk_slice[key + 3] * p.sk_mul : 0.0f;
+                    }
                     reinterpret_cast<float4*>(sm.sk[st])[lane] = kv4;
                     if (lane == 0) {
                         mbar_arrive_expect_tx(&sm.k_full[st], kKBytes);
@@ -271,7 +298,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         for (int kk = 0; kk < D / 32; ++kk) {
                             const uint64_t adesc = smem_desc(q_base + kk * 32, 16, kSbo, kLayout);
                             const uint64_t bdesc = smem_desc(k_base + kk * 32, 16, kSbo, kLayout);
-                            mma_i8_ss(tmem + T_S, adesc, bdesc, kIdescS, kk > 0 ? 1u : 0u);
+                            if constexpr (FP8)
+                                mma_f8_ss(tmem + T_S, adesc, bdesc, kIdescS, kk > 0 ? 1u : 0u);
+                            else
+                                mma_i8_ss(tmem + T_S, adesc, bdesc, kIdescS, kk > 0 ? 1u : 0u);
                         }
                         mma_commit_u32(b_s_full);
                         if (have_prev) issue_pv(prev_st, prev_ph, pi++);
@@ -309,7 +339,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int32_t q0 = (idx % p.q_tiles) * BM, slice = idx / p.q_tiles;
             const int32_t grow = q0 + row;
             const bool row_ok = grow < n;
-            const float sq_r = row_ok ? p.sq[static_cast<int64_t>(slice) * n + grow] : 0.0f;
+            const float sq_r =
+                FP8 ? 1.0f : (row_ok ? p.sq[static_cast<int64_t>(slice) * n + grow] : 0.0f);
             float acc[NCOL];
 #pragma unroll
             for (int c = 0; c < NCOL; ++c) acc[c] = 0.0f;
@@ -359,12 +390,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int c4 = 0; c4 < NCOL / 4; ++c4) {
                     const float4 k4 = sk4[c4];
                     const int c = 4 * c4;
-                    const float2 a = fmul2(make_float2(__int2float_rn(static_cast<int32_t>(sr[c])),
-                                                       __int2float_rn(static_cast<int32_t>(sr[c + 1]))),
-                                           make_float2(k4.x, k4.y));
-                    const float2 b = fmul2(make_float2(__int2float_rn(static_cast<int32_t>(sr[c + 2])),
-                                                       __int2float_rn(static_cast<int32_t>(sr[c + 3]))),
-                                           make_float2(k4.z, k4.w));
+                    float2 sa, sb;  // S as f32: exact int32 (kind::i8) or f32 (kind::f8f6f4)
+                    if constexpr (FP8) {
+                        sa = make_float2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
+                        sb = make_float2(__uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
+                    } else {
+                        sa = make_float2(__int2float_rn(static_cast<int32_t>(sr[c])),
+                                         __int2float_rn(static_cast<int32_t>(sr[c + 1])));
+                        sb = make_float2(__int2float_rn(static_cast<int32_t>(sr[c + 2])),
+                                         __int2float_rn(static_cast<int32_t>(sr[c + 3])));
+                    }
+                    const float2 a = fmul2(sa, make_float2(k4.x, k4.y));
+                    const float2 b = fmul2(sb, make_float2(k4.z, k4.w));
                     u[c] = a.x;
                     u[c + 1] = a.y;
                     u[c + 2] = b.x;
@@ -439,7 +476,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             fold(pend_alpha);
             // O = acc * (1/l)  (finalize_softmax_state, attention.cpp:139-149)
             if (row_ok && c_base < p.d) {
-                const float inv = __fdiv_rn(1.0f, l);
+                // FP8: V was restored as decode(code) / sV (fp8.cpp:94)
+                const float inv =
+                    FP8 ? __fdiv_rn(__fdiv_rn(1.0f, l), p.sv[slice]) : __fdiv_rn(1.0f, l);
                 float* orow = p.o + (static_cast<int64_t>(slice) * n + grow) * p.d + c_base;
                 if (p.d % 4 == 0 && c_base + NCOL <= p.d) {
 #pragma unroll
@@ -508,10 +547,10 @@ static bool make_map(CUtensorMap* map, const void* base, CUtensorMapDataType dt,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int D>
-static cudaError_t launch(const int8_t* q, const float* sq, const int8_t* k, const float* sk,
-                          const uint16_t* v, float* o, int64_t slices, int64_t n, int64_t d,
-                          int64_t pitch, bool sqrt_d, cudaStream_t stream) {
+template <int D, bool FP8>
+static cudaError_t launch(const uint8_t* q, const float* sq, const uint8_t* k, const float* sk,
+                          const uint16_t* v, const float* sv, float* o, int64_t slices,
+                          int64_t n, int64_t d, int64_t pitch, bool sqrt_d, cudaStream_t stream) {
     CUtensorMap tq, tk, tv;
     const CUtensorMapSwizzle sw8 = D == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
     if (!make_map(&tq, q, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, slices, n, pitch, D, sw8) ||
@@ -522,6 +561,7 @@ static cudaError_t launch(const int8_t* q, const float* sq, const int8_t* k, con
     Params p;
     p.sq = sq;
     p.sk = sk;
+    p.sv = sv;
     p.o = o;
     p.n = static_cast<int32_t>(n);
     p.d = static_cast<int32_t>(d);
@@ -532,7 +572,7 @@ static cudaError_t launch(const int8_t* q, const float* sq, const int8_t* k, con
     const size_t smem = sizeof(Smem<D>) + 1024;
     static bool configured = false;
     if (!configured) {
-        const cudaError_t e = cudaFuncSetAttribute(half_int8_fwd_kernel<D>,
+        const cudaError_t e = cudaFuncSetAttribute(half_int8_fwd_kernel<D, FP8>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    static_cast<int>(smem));
         if (e != cudaSuccess) return e;
@@ -546,7 +586,7 @@ static cudaError_t launch(const int8_t* q, const float* sq, const int8_t* k, con
         if (sms <= 0) sms = 148;
     }
     const int grid = p.items < sms ? p.items : sms;
-    half_int8_fwd_kernel<D><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+    half_int8_fwd_kernel<D, FP8><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
     return cudaGetLastError();
 }
 
@@ -556,9 +596,27 @@ cudaError_t launch_half_int8_fwd(const int8_t* q, const float* sq, const int8_t*
                                  const float* sk, const uint16_t* v, float* o, int64_t slices,
                                  int64_t n, int64_t d, int64_t pitch, bool sqrt_d,
                                  cudaStream_t stream) {
-    if (d == 64) return halfk::launch<64>(q, sq, k, sk, v, o, slices, n, d, pitch, sqrt_d, stream);
+    const uint8_t* q8 = reinterpret_cast<const uint8_t*>(q);
+    const uint8_t* k8 = reinterpret_cast<const uint8_t*>(k);
+    if (d == 64)
+        return halfk::launch<64, false>(q8, sq, k8, sk, v, nullptr, o, slices, n, d, pitch, sqrt_d,
+                                        stream);
     if (d == 128)
-        return halfk::launch<128>(q, sq, k, sk, v, o, slices, n, d, pitch, sqrt_d, stream);
+        return halfk::launch<128, false>(q8, sq, k8, sk, v, nullptr, o, slices, n, d, pitch,
+                                         sqrt_d, stream);
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_fp8_attention_fwd(const uint8_t* q, const float* q_scales, const uint8_t* k,
+                                     const float* k_scales, const uint16_t* v,
+                                     const float* v_scales, float* o, int64_t slices, int64_t n,
+                                     int64_t d, bool sqrt_d, cudaStream_t stream) {
+    if (d == 64)
+        return halfk::launch<64, true>(q, q_scales, k, k_scales, v, v_scales, o, slices, n, d, d,
+                                       sqrt_d, stream);
+    if (d == 128)
+        return halfk::launch<128, true>(q, q_scales, k, k_scales, v, v_scales, o, slices, n, d,
+                                        d, sqrt_d, stream);
     return cudaErrorInvalidValue;
 }
 

@@ -56,5 +56,15 @@ cudaError_t launch_half_int8_fwd(const int8_t* q, const float* sq, const int8_t*
                                  int64_t n, int64_t d, int64_t pitch, bool sqrt_d,
                                  cudaStream_t stream);
 cudaError_t launch_convert_f16(const float* x, int64_t count, uint16_t* out, cudaStream_t stream);
+// per-slice e4m3 codes (+ decoded fp16) and the FP8 forward
+// (attn_half.cu with S via kind::f8f6f4); d in {64, 128}, V = decoded fp16.
+cudaError_t launch_fp8_quantize_per_tensor(const float* x, int64_t slices, int64_t rows,
+                                           int64_t cols, uint8_t* codes, uint16_t* decoded,
+                                           float* slice_scales, uint32_t* amax_ws, int64_t* bad,
+                                           cudaStream_t stream);
+cudaError_t launch_fp8_attention_fwd(const uint8_t* q, const float* q_scales, const uint8_t* k,
+                                     const float* k_scales, const uint16_t* v,
+                                     const float* v_scales, float* o, int64_t slices, int64_t n,
+                                     int64_t d, bool sqrt_d, cudaStream_t stream);
 
 }  // namespace ifa_b200

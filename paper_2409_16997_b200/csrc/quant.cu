@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cooperative_groups.h>
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "ifa_internal.h"
@@ -213,6 +214,42 @@ __global__ void __launch_bounds__(256) slice_quantize_kernel(const float* __rest
         }
     } else {
         for (int64_t i = tid; i < slice_elems; i += stride) dst[i] = quantize_one(src[i], scale);
+    }
+}
+
+// FP8 e4m3 per-slice roundtrip codes (fp8.cpp:78-97): s = 448 / max|x|, code
+// = e4m3(RN(x * s)) with the hardware's round-to-nearest-even, saturating
+// conversion (the reference's e4m3_encode: ties to even, saturate at 448,
+// subnormal step 2^-9).  Optionally also the decoded values as fp16 (exact).
+__global__ void __launch_bounds__(256) slice_fp8_kernel(const float* __restrict__ x,
+                                                        int64_t slice_elems,
+                                                        const uint32_t* __restrict__ amax,
+                                                        uint8_t* __restrict__ codes,
+                                                        __half* __restrict__ decoded,
+                                                        float* __restrict__ slice_scales) {
+    const int64_t s = blockIdx.y;
+    const float mx = __uint_as_float(amax[s]);
+    const float scale = mx == 0.0f ? 0.0f : __fdiv_rn(448.0f, mx);
+    if (blockIdx.x == 0 && threadIdx.x == 0) slice_scales[s] = scale;
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t n2 = slice_elems >> 1;  // slice_elems is even (host check)
+    const float2* s2 = reinterpret_cast<const float2*>(x + s * slice_elems);
+    uint16_t* c2 = reinterpret_cast<uint16_t*>(codes + s * slice_elems);
+    __half2* h2 = decoded ? reinterpret_cast<__half2*>(decoded + s * slice_elems) : nullptr;
+    for (int64_t i = tid; i < n2; i += stride) {
+        const float2 v = __ldcs(s2 + i);
+        uint16_t pair;
+        // e4m3x2: first operand -> high byte
+        asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;"
+            : "=h"(pair)
+            : "f"(__fmul_rn(v.y, scale)), "f"(__fmul_rn(v.x, scale)));
+        c2[i] = pair;
+        if (h2) {
+            uint32_t hh;
+            asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(hh) : "h"(pair));
+            h2[i] = *reinterpret_cast<const __half2*>(&hh);
+        }
     }
 }
 
@@ -436,6 +473,34 @@ cudaError_t launch_quantize_per_tensor(const float* x, int64_t slices, int64_t r
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
     slice_quantize_kernel<<<grid, threads, 0, stream>>>(x, elems, amax_ws, codes, slice_scales, vec);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fp8_quantize_per_tensor(const float* x, int64_t slices, int64_t rows,
+                                           int64_t cols, uint8_t* codes, uint16_t* decoded,
+                                           float* slice_scales, uint32_t* amax_ws, int64_t* bad,
+                                           cudaStream_t stream) {
+    const int64_t elems = rows * cols;
+    if (slices == 0 || elems == 0) return cudaSuccess;
+    if (elems % 2 != 0 || slices > 65535 || reinterpret_cast<uintptr_t>(x) % 8 != 0 ||
+        reinterpret_cast<uintptr_t>(codes) % 2 != 0 ||
+        reinterpret_cast<uintptr_t>(decoded) % 4 != 0)
+        return cudaErrorInvalidValue;
+    cudaError_t err = cudaMemsetAsync(amax_ws, 0, sizeof(uint32_t) * slices, stream);
+    if (err != cudaSuccess) return err;
+    const int threads = 256;
+    const int vec = (elems % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+    int64_t per_slice = (static_cast<int64_t>(sm_count()) * 8 + slices - 1) / slices;
+    const int64_t max_useful = (elems / 2 + threads * 4 - 1) / (threads * 4);
+    if (per_slice > max_useful) per_slice = max_useful;
+    if (per_slice < 1) per_slice = 1;
+    dim3 grid(static_cast<unsigned>(per_slice), static_cast<unsigned>(slices));
+    slice_absmax_kernel<<<grid, threads, 0, stream>>>(x, elems, amax_ws, bad, vec);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+    slice_fp8_kernel<<<grid, threads, 0, stream>>>(x, elems, amax_ws, codes,
+                                                   reinterpret_cast<__half*>(decoded),
+                                                   slice_scales);
     return cudaGetLastError();
 }
 

@@ -41,6 +41,11 @@ APPENDIX_B_HALF = {
     "normal": {1024: 2.01, 2048: 2.30, 4096: 2.41, 8192: 2.52, 16384: 2.56},
     "uniform": {1024: 0.496, 2048: 0.498, 4096: 0.514, 8192: 0.523, 16384: 0.514},
 }
+# reference fp8_emulated_attention MRE vs fp64.
+APPENDIX_B_FP8 = {
+    "normal": {1024: 9.49, 2048: 10.5, 4096: 11.2, 8192: 11.5, 16384: 11.8},
+    "uniform": {1024: 4.17, 2048: 4.13, 4096: 4.22, 8192: 4.34, 16384: 4.25},
+}
 # Paper tables (RTX 4090, Triton; shape details unstated): PAPER.md:163-187.
 PAPER = {
     "normal": {1024: 4.05, 2048: 4.18, 4096: 4.21, 8192: 4.38, 16384: 4.52},
@@ -82,6 +87,11 @@ def run_case(o, dist, n, d, seed_idx, outlier=None):
     acc = ErrorAccum()
     acc.add(ref, half_forward(q, k, v))
     res["half"] = acc
+    acc = ErrorAccum()
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    acc.add(ref, ifa.fp8_emulated_attention(dev(q), dev(k), dev(v),
+                                            ifa.AttentionConfig(ifa.BlockSpec(128, 128))))
+    res["fp8"] = acc
     return res
 
 
@@ -102,13 +112,15 @@ def main():
                          "mre_exact_pct": 100 * r["exact"].ratio(),
                          "mre_fast_pct": 100 * r["fast"].ratio(),
                          "mre_half_pct": 100 * r["half"].ratio(),
+                         "mre_fp8_pct": 100 * r["fp8"].ratio(),
                          "appendix_b_pct": APPENDIX_B[dist][n], "paper_pct": PAPER[dist][n],
-                         "appendix_b_half_pct": APPENDIX_B_HALF[dist][n]})
+                         "appendix_b_half_pct": APPENDIX_B_HALF[dist][n],
+                         "appendix_b_fp8_pct": APPENDIX_B_FP8[dist][n]})
     settings = [("x10 in Q,K,V", (10.0, (0, 1, 2))), ("x100 in Q,K,V", (100.0, (0, 1, 2))),
                 ("x10 in Q,K only", (10.0, (0, 1))), ("x10 in V only", (10.0, (2,)))]
     for dist in ("normal", "uniform"):
         for label, spec in settings:
-            per_seed = {"exact": [], "fast": [], "half": []}
+            per_seed = {"exact": [], "fast": [], "half": [], "fp8": []}
             for seed_idx in (21, 22, 23):
                 r = run_case(o, dist, 1024, d, seed_idx, outlier=spec)
                 for m in per_seed:
@@ -116,7 +128,8 @@ def main():
             rows.append({"dist": dist, "n": 1024, "outliers": label,
                          "mre_exact_pct": 100 * float(np.mean(per_seed["exact"])),
                          "mre_fast_pct": 100 * float(np.mean(per_seed["fast"])),
-                         "mre_half_pct": 100 * float(np.mean(per_seed["half"]))})
+                         "mre_half_pct": 100 * float(np.mean(per_seed["half"])),
+                         "mre_fp8_pct": 100 * float(np.mean(per_seed["fp8"]))})
     wall = time.time() - t0
     with open(args.out + ".json", "w") as f:
         json.dump({"rows": rows, "wall_s": wall, "d": d, "bc": 128,
@@ -126,12 +139,14 @@ def main():
                   indent=1)
     lines = ["| dist | N | outliers | full-INT8 exact (%) | full-INT8 fast (%) | "
              "reference full-INT8, App. B (%) | paper full-INT8, RTX 4090 (%) | half-INT8 (%) | "
-             "reference half-INT8, App. B (%) |", "|---|---|---|---|---|---|---|---|---|"]
+             "reference half-INT8, App. B (%) | FP8 e4m3 (%) | reference FP8, App. B (%) |",
+             "|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         lines.append(f"| {r['dist']} | {r['n']} | {r['outliers']} | {r['mre_exact_pct']:.3f} | "
                      f"{r['mre_fast_pct']:.3f} | {r.get('appendix_b_pct', '')} | "
                      f"{r.get('paper_pct', '')} | {r['mre_half_pct']:.3f} | "
-                     f"{r.get('appendix_b_half_pct', '')} |")
+                     f"{r.get('appendix_b_half_pct', '')} | {r['mre_fp8_pct']:.3f} | "
+                     f"{r.get('appendix_b_fp8_pct', '')} |")
     with open(args.out + ".md", "w") as f:
         f.write("\n".join(lines) + f"\n\nwall {wall:.1f} s on one B200\n")
     print("\n".join(lines))
