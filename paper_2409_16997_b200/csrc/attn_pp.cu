@@ -193,7 +193,7 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uin
         : "memory");
 }
 
-template <int D>
+template <int D, bool CAUSAL>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     int_flash_pp_kernel(const __grid_constant__ CUtensorMap tm_q,
                         const __grid_constant__ CUtensorMap tm_k,
@@ -209,7 +209,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t lane = lane_id();
     const int32_t n = p.n;
     const int32_t J = n / BN;  // KV tiles of a slice (n % 128 == 0)
-    const bool causal = (p.flags & IFA_FLAG_CAUSAL) != 0;
+    // compile-time: the non-causal instantiation carries no masking or
+    // per-group tile-count logic (it measured 20% slower with them at run time)
+    constexpr bool causal = CAUSAL;
 
     const uint32_t b_q_full = smem_u32(&sm.q_full), b_q_empty = smem_u32(&sm.q_empty);
     const uint32_t b_k_full = smem_u32(&sm.k_full[0]), b_k_empty = smem_u32(&sm.k_empty[0]);
@@ -735,9 +737,13 @@ static cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     const size_t smem = sizeof(Smem<D>) + 1024;
     static bool configured = false;
     if (!configured) {
-        e = cudaFuncSetAttribute(int_flash_pp_kernel<D>,
+        e = cudaFuncSetAttribute(int_flash_pp_kernel<D, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(int_flash_pp_kernel<D, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem));
         if (e != cudaSuccess) {
             cudaFreeAsync(v16, stream);
             return e;
@@ -752,7 +758,10 @@ static cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
         if (sms <= 0) sms = 148;
     }
     const int grid = p.items < sms ? p.items : sms;
-    int_flash_pp_kernel<D><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+    if (a.flags & IFA_FLAG_CAUSAL)
+        int_flash_pp_kernel<D, true><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+    else
+        int_flash_pp_kernel<D, false><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
     e = cudaGetLastError();
     const cudaError_t e2 = cudaFreeAsync(v16, stream);
     return e != cudaSuccess ? e : e2;
