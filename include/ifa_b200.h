@@ -103,6 +103,22 @@ int ifa_int_flash_fwd(const int8_t* q, const float* sq, const int8_t* k, const f
                       int64_t d, int64_t br, int64_t bc, uint32_t flags,
                       ifa_pcode_audit* audit, void* stream);
 
+/* ---- fp16 V codes for the two-Q-tile tolerance kernel --------------------
+ * ifa_quantize_per_tensor_v16: ifa_quantize_per_tensor that also writes the
+ *   V codes as fp16 (codes_f16, same [slices][rows][cols] layout, exact),
+ *   fused into the quantizer's second pass.
+ * ifa_int_flash_fwd_v16: ifa_int_flash_fwd with those fp16 codes supplied,
+ *   so the two-Q-tile kernel (IFA_FLAG_FAST, Bc = 128, n % 128 == 0, d in
+ *   {64, 128}; csrc/attn_pp.cu) skips its own conversion.  Any other case
+ *   runs exactly ifa_int_flash_fwd on the int8 v (no audit). */
+int ifa_quantize_per_tensor_v16(const float* x, int64_t slices, int64_t rows, int64_t cols,
+                                int8_t* codes, uint16_t* codes_f16, float* slice_scales,
+                                void* workspace, int64_t* nonfinite_index, void* stream);
+int ifa_int_flash_fwd_v16(const int8_t* q, const float* sq, const int8_t* k, const float* sk,
+                          const int8_t* v, const uint16_t* v_f16, const float* sv, float* o,
+                          int64_t slices, int64_t n, int64_t d, int64_t br, int64_t bc,
+                          uint32_t flags, void* stream);
+
 /* ---- half-INT8 attention ----------------------------
  * ifa_half_int8_fwd  replaces ifa::half_int8_attention (attention.hpp:93-96,
  *                    attention.cpp:359-399): int8 Q/K with per-row scales

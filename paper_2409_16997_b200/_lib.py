@@ -30,6 +30,8 @@ EXPORTED_SYMBOLS = (
     "ifa_int_flash_fwd",
     "ifa_half_int8_fwd",
     "ifa_convert_f16",
+    "ifa_quantize_per_tensor_v16",
+    "ifa_int_flash_fwd_v16",
     "ifa_fp8_quantize_per_tensor",
     "ifa_fp8_attention_fwd",
     "ifa_quantize_per_row_host",
@@ -89,6 +91,11 @@ def load() -> C.CDLL:
     lib.ifa_half_int8_fwd.restype = C.c_int
     lib.ifa_convert_f16.argtypes = [vp, i64, vp, vp]
     lib.ifa_convert_f16.restype = C.c_int
+    lib.ifa_quantize_per_tensor_v16.argtypes = [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp]
+    lib.ifa_quantize_per_tensor_v16.restype = C.c_int
+    lib.ifa_int_flash_fwd_v16.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i64,
+                                          i64, u32, vp]
+    lib.ifa_int_flash_fwd_v16.restype = C.c_int
     lib.ifa_fp8_quantize_per_tensor.argtypes = [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp]
     lib.ifa_fp8_quantize_per_tensor.restype = C.c_int
     lib.ifa_fp8_attention_fwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64,

@@ -179,6 +179,49 @@ int ifa_int_flash_fwd(const int8_t* q, const float* sq, const int8_t* k, const f
     return e == cudaSuccess ? IFA_OK : cuda_fail(e, "int_flash_attention");
 }
 
+int ifa_quantize_per_tensor_v16(const float* x, int64_t slices, int64_t rows, int64_t cols,
+                                int8_t* codes, uint16_t* codes_f16, float* slice_scales,
+                                void* workspace, int64_t* nonfinite_index, void* stream) {
+    g_err.clear();
+    if (slices < 0 || rows < 0 || cols < 0)
+        return fail(IFA_EINVAL, "quantize_per_tensor: negative matrix extent");
+    if (slices == 0) return IFA_OK;
+    if (!slice_scales || !workspace || !codes_f16)
+        return fail(IFA_EINVAL, "quantize_per_tensor: null pointer");
+    if (rows == 0 || cols == 0) {
+        const cudaError_t e = cudaMemsetAsync(slice_scales, 0, sizeof(float) * slices,
+                                              static_cast<cudaStream_t>(stream));
+        return e == cudaSuccess ? IFA_OK : cuda_fail(e, "quantize_per_tensor");
+    }
+    if (!x || !codes) return fail(IFA_EINVAL, "quantize_per_tensor: null pointer");
+    const cudaError_t e = ifa_b200::launch_quantize_per_tensor(
+        x, slices, rows, cols, codes, slice_scales, static_cast<uint32_t*>(workspace),
+        nonfinite_index, static_cast<cudaStream_t>(stream), codes_f16);
+    return e == cudaSuccess ? IFA_OK : cuda_fail(e, "quantize_per_tensor");
+}
+
+int ifa_int_flash_fwd_v16(const int8_t* q, const float* sq, const int8_t* k, const float* sk,
+                          const int8_t* v, const uint16_t* v_f16, const float* sv, float* o,
+                          int64_t slices, int64_t n, int64_t d, int64_t br, int64_t bc,
+                          uint32_t flags, void* stream) {
+    g_err.clear();
+    const int rc = ifa_b200::validate_fwd(slices, n, d, br, bc, flags);
+    if (rc != IFA_OK) return rc;
+    if (slices == 0) return IFA_OK;
+    if (!q || !sq || !k || !sk || !v || !v_f16 || !sv || !o)
+        return fail(IFA_EINVAL, "int_flash_attention: null pointer");
+    ifa_b200::AttnArgs a{q, sq, k, sk, v, sv, o, nullptr, slices, n, d, d, bc, flags};
+    const bool aligned = ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) |
+                           reinterpret_cast<uintptr_t>(v_f16)) % 16) == 0;
+    if ((d == 64 || d == 128) && aligned && ifa_b200::int_flash_pp_eligible(a)) {
+        const cudaError_t e =
+            ifa_b200::launch_int_flash_pp(a, v_f16, static_cast<cudaStream_t>(stream));
+        return e == cudaSuccess ? IFA_OK : cuda_fail(e, "int_flash_attention");
+    }
+    return ifa_int_flash_fwd(q, sq, k, sk, v, sv, o, slices, n, d, br, bc, flags, nullptr,
+                             stream);
+}
+
 int ifa_half_int8_fwd(const int8_t* q, const float* sq, const int8_t* k, const float* sk,
                       const uint16_t* v_f16, float* o, int64_t slices, int64_t n, int64_t d,
                       int64_t br, int64_t bc, uint32_t flags, void* stream) {

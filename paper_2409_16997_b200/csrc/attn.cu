@@ -1338,7 +1338,7 @@ static cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
 cudaError_t launch_int_flash_fwd(const AttnArgs& a, cudaStream_t stream) {
     if (a.n > (int64_t{1} << 30) || ((a.n + 127) / 128) * a.slices > INT32_MAX)
         return cudaErrorInvalidValue;
-    if (int_flash_pp_eligible(a)) return launch_int_flash_pp(a, stream);
+    if (int_flash_pp_eligible(a)) return launch_int_flash_pp(a, nullptr, stream);
     if (a.d <= 64) return attn::launch_d<64>(a, stream);
     return attn::launch_d<128>(a, stream);
 }

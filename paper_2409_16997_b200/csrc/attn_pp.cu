@@ -693,7 +693,7 @@ static bool make_map_v16(CUtensorMap* map, const __half* base, int64_t slices, i
 }
 
 template <int D>
-static cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
+static cudaError_t launch(const AttnArgs& a, const uint16_t* v16_given, cudaStream_t stream) {
     static bool pool_kept = false;
     if (!pool_kept) {  // keep the per-call fp16 V workspace in the stream-ordered pool
         int dev = 0;
@@ -704,11 +704,14 @@ static cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
         }
         pool_kept = true;
     }
-    __half* v16 = nullptr;
+    __half* v16 = const_cast<__half*>(reinterpret_cast<const __half*>(v16_given));
+    __half* owned = nullptr;
     const int64_t rows = a.slices * a.n;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&v16), rows * D * 2, stream);
-    if (e != cudaSuccess) return e;
-    {
+    cudaError_t e = cudaSuccess;
+    if (!v16) {  // fp16 copy of the V codes (the caller may pass one: ifa_int_flash_fwd_v16)
+        e = cudaMallocAsync(reinterpret_cast<void**>(&owned), rows * D * 2, stream);
+        if (e != cudaSuccess) return e;
+        v16 = owned;
         int64_t blocks = (rows * D / 8 + 255) / 256;
         if (blocks > 148 * 16) blocks = 148 * 16;
         codes_to_f16_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(a.v, rows, a.pitch,
@@ -718,7 +721,7 @@ static cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     if (!make_map_codes(&tq, a.q, a.slices, a.n, a.pitch, D) ||
         !make_map_codes(&tk, a.k, a.slices, a.n, a.pitch, D) ||
         !make_map_v16(&tv, v16, a.slices, a.n, D)) {
-        cudaFreeAsync(v16, stream);
+        if (owned) cudaFreeAsync(owned, stream);
         return cudaErrorInvalidValue;
     }
     Params p;
@@ -745,7 +748,7 @@ static cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem));
         if (e != cudaSuccess) {
-            cudaFreeAsync(v16, stream);
+            if (owned) cudaFreeAsync(owned, stream);
             return e;
         }
         configured = true;
@@ -763,7 +766,7 @@ static cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     else
         int_flash_pp_kernel<D, false><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
     e = cudaGetLastError();
-    const cudaError_t e2 = cudaFreeAsync(v16, stream);
+    const cudaError_t e2 = owned ? cudaFreeAsync(owned, stream) : cudaSuccess;
     return e != cudaSuccess ? e : e2;
 }
 
@@ -784,9 +787,9 @@ bool int_flash_pp_eligible(const AttnArgs& a) {
            a.audit == nullptr && tiles_are_blocks && a.n % 128 == 0 && a.d <= 128;
 }
 
-cudaError_t launch_int_flash_pp(const AttnArgs& a, cudaStream_t stream) {
-    if (a.d <= 64) return pp::launch<64>(a, stream);
-    return pp::launch<128>(a, stream);
+cudaError_t launch_int_flash_pp(const AttnArgs& a, const uint16_t* v16, cudaStream_t stream) {
+    if (a.d <= 64) return pp::launch<64>(a, v16, stream);
+    return pp::launch<128>(a, v16, stream);
 }
 
 }  // namespace ifa_b200

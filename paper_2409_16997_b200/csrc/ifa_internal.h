@@ -21,7 +21,8 @@ cudaError_t launch_quantize_per_row(const float* x, int64_t rows, int64_t cols, 
                                     float* scales, int64_t* bad, cudaStream_t stream);
 cudaError_t launch_quantize_per_tensor(const float* x, int64_t slices, int64_t rows,
                                        int64_t cols, int8_t* codes, float* slice_scales,
-                                       uint32_t* amax_ws, int64_t* bad, cudaStream_t stream);
+                                       uint32_t* amax_ws, int64_t* bad, cudaStream_t stream,
+                                       uint16_t* codes_f16 = nullptr);
 
 struct AttnArgs {
     const int8_t* q;
@@ -47,7 +48,9 @@ cudaError_t launch_int_flash_fwd(const AttnArgs& a, cudaStream_t stream);
 // attn_pp.cu: tolerance-mode kernel with two Q tiles per CTA (non-causal,
 // 128-key blocks, n % 16 == 0); IFA_B200_NO_PP=1 disables it.
 bool int_flash_pp_eligible(const AttnArgs& a);
-cudaError_t launch_int_flash_pp(const AttnArgs& a, cudaStream_t stream);
+// v16: [slices][n][D] fp16 copy of the V codes (D = 64 for d <= 64, else
+// 128), or null to convert a.v internally.
+cudaError_t launch_int_flash_pp(const AttnArgs& a, const uint16_t* v16, cudaStream_t stream);
 
 // attn_half.cu: half-INT8 forward (q/k codes of row pitch `pitch`, v fp16
 // [slices][n][d] dense, d in {64, 128}) and the f32 -> fp16 conversion.

@@ -309,10 +309,25 @@ __global__ void __launch_bounds__(256) quantize_rows8_kernel(const float* __rest
 // CTA's chunk; the cluster combines the partials through DSMEM.  Pass 2:
 // quantize the chunk, re-read from L2.
 constexpr int kSliceCluster = 8;
+
+// Four packed int8 codes -> four fp16 (exact), for the two-Q-tile attention
+// kernel's P.V operand.
+__device__ __forceinline__ uint2 codes4_to_f16(uint32_t w) {
+    const __half2 lo = __halves2half2(__int2half_rn(static_cast<int8_t>(w & 0xff)),
+                                      __int2half_rn(static_cast<int8_t>((w >> 8) & 0xff)));
+    const __half2 hi = __halves2half2(__int2half_rn(static_cast<int8_t>((w >> 16) & 0xff)),
+                                      __int2half_rn(static_cast<int8_t>(w >> 24)));
+    return make_uint2(*reinterpret_cast<const uint32_t*>(&lo),
+                      *reinterpret_cast<const uint32_t*>(&hi));
+}
+
+// F16: also write the codes as fp16 (codes16, same layout).
+template <bool F16>
 __global__ void __cluster_dims__(kSliceCluster, 1, 1) __launch_bounds__(512)
     slice_quantize_fused_kernel(const float* __restrict__ x, int64_t slices,
                                 int64_t slice_elems, int8_t* __restrict__ codes,
-                                float* __restrict__ slice_scales, int64_t* bad) {
+                                float* __restrict__ slice_scales, int64_t* bad,
+                                uint16_t* __restrict__ codes16) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     __shared__ float red[16];
@@ -382,18 +397,33 @@ __global__ void __cluster_dims__(kSliceCluster, 1, 1) __launch_bounds__(512)
         const float rcp = __frcp_rn(scale);
         const bool exact_row = !(rcp <= 3.402823466e38f);
         uint32_t* dst = reinterpret_cast<uint32_t*>(codes + slice * slice_elems);
+        uint2* dst16 = F16 ? reinterpret_cast<uint2*>(codes16 + slice * slice_elems) : nullptr;
         {
             const int64_t stride = blockDim.x;
             int64_t i = lo + threadIdx.x;
             for (; i + 3 * stride < hi; i += 4 * stride) {
                 const float4 a = __ldcs(src + i), b = __ldcs(src + i + stride),
                              c = __ldcs(src + i + 2 * stride), d = __ldcs(src + i + 3 * stride);
-                dst[i] = codes4(a, scale, rcp, exact_row);
-                dst[i + stride] = codes4(b, scale, rcp, exact_row);
-                dst[i + 2 * stride] = codes4(c, scale, rcp, exact_row);
-                dst[i + 3 * stride] = codes4(d, scale, rcp, exact_row);
+                const uint32_t wa = codes4(a, scale, rcp, exact_row);
+                const uint32_t wb = codes4(b, scale, rcp, exact_row);
+                const uint32_t wc = codes4(c, scale, rcp, exact_row);
+                const uint32_t wd = codes4(d, scale, rcp, exact_row);
+                dst[i] = wa;
+                dst[i + stride] = wb;
+                dst[i + 2 * stride] = wc;
+                dst[i + 3 * stride] = wd;
+                if constexpr (F16) {
+                    dst16[i] = codes4_to_f16(wa);
+                    dst16[i + stride] = codes4_to_f16(wb);
+                    dst16[i + 2 * stride] = codes4_to_f16(wc);
+                    dst16[i + 3 * stride] = codes4_to_f16(wd);
+                }
             }
-            for (; i < hi; i += stride) dst[i] = codes4(__ldcs(src + i), scale, rcp, exact_row);
+            for (; i < hi; i += stride) {
+                const uint32_t w = codes4(__ldcs(src + i), scale, rcp, exact_row);
+                dst[i] = w;
+                if constexpr (F16) dst16[i] = codes4_to_f16(w);
+            }
         }
         __syncthreads();  // red[] reuse
     }
@@ -440,9 +470,17 @@ cudaError_t launch_quantize_per_row(const float* x, int64_t rows, int64_t cols, 
     return cudaGetLastError();
 }
 
+__global__ void codes_i8_to_f16_kernel(const int8_t* __restrict__ src, int64_t count,
+                                       __half* __restrict__ dst) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += stride)
+        dst[i] = __int2half_rn(src[i]);
+}
+
 cudaError_t launch_quantize_per_tensor(const float* x, int64_t slices, int64_t rows, int64_t cols,
                                        int8_t* codes, float* slice_scales, uint32_t* amax_ws,
-                                       int64_t* bad, cudaStream_t stream) {
+                                       int64_t* bad, cudaStream_t stream, uint16_t* codes_f16) {
     if (slices == 0 || rows == 0 || cols == 0) return cudaSuccess;
     const int64_t elems = rows * cols;
     const int vec = (elems % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
@@ -455,8 +493,18 @@ cudaError_t launch_quantize_per_tensor(const float* x, int64_t slices, int64_t r
         const int64_t min_clusters = (sm_count() + kSliceCluster - 1) / kSliceCluster + 1;
         if (nclusters < min_clusters) nclusters = min_clusters;
         if (nclusters > slices) nclusters = slices;
-        slice_quantize_fused_kernel<<<static_cast<unsigned>(nclusters * kSliceCluster), 512, 0,
-                                      stream>>>(x, slices, elems, codes, slice_scales, bad);
+        const unsigned grid = static_cast<unsigned>(nclusters * kSliceCluster);
+        if (codes_f16 && reinterpret_cast<uintptr_t>(codes_f16) % 8 == 0)
+            slice_quantize_fused_kernel<true><<<grid, 512, 0, stream>>>(
+                x, slices, elems, codes, slice_scales, bad, codes_f16);
+        else
+            slice_quantize_fused_kernel<false><<<grid, 512, 0, stream>>>(
+                x, slices, elems, codes, slice_scales, bad, nullptr);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess || !codes_f16 || reinterpret_cast<uintptr_t>(codes_f16) % 8 == 0)
+            return e;
+        codes_i8_to_f16_kernel<<<148 * 8, 256, 0, stream>>>(codes, slices * elems,
+                                                             reinterpret_cast<__half*>(codes_f16));
         return cudaGetLastError();
     }
     cudaError_t err = cudaMemsetAsync(amax_ws, 0, sizeof(uint32_t) * slices, stream);
@@ -473,6 +521,10 @@ cudaError_t launch_quantize_per_tensor(const float* x, int64_t slices, int64_t r
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
     slice_quantize_kernel<<<grid, threads, 0, stream>>>(x, elems, amax_ws, codes, slice_scales, vec);
+    err = cudaGetLastError();
+    if (err != cudaSuccess || !codes_f16) return err;
+    codes_i8_to_f16_kernel<<<148 * 8, 256, 0, stream>>>(codes, slices * elems,
+                                                         reinterpret_cast<__half*>(codes_f16));
     return cudaGetLastError();
 }
 

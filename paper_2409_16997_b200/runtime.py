@@ -32,6 +32,8 @@ class AttentionPlan:
             raise ValueError("BlockSpec: Br and Bc must be >= 1")
         self.lib = _lib.load()
         dev = torch.device(device) if device is not None else torch.device("cuda")
+        if dev.type == "cuda" and dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
         self.device = dev
         self.slices, self.n, self.d, self.bc, self.br = slices, n, d, bc, br
         self.flags = (_lib.FLAG_CAUSAL if causal else 0) | (_lib.FLAG_SQRT_D if sqrt_d else 0) | \
@@ -46,6 +48,9 @@ class AttentionPlan:
         self.out = torch.empty(shape, dtype=torch.float32, device=dev)
         self.ws = torch.empty((slices,), dtype=torch.int32, device=dev)
         self.bad = torch.full((1,), _INT64_MAX, dtype=torch.int64, device=dev)
+        # fp16 V codes for the two-Q-tile kernel, written by the V quantizer
+        self.v16 = torch.empty(shape, dtype=torch.float16, device=dev) \
+            if self.uses_pp_kernel() and d in (64, 128) else None
         self.graph: Optional[torch.cuda.CUDAGraph] = None
         self._graph_io = None
 
@@ -59,12 +64,24 @@ class AttentionPlan:
                                           self.sq.data_ptr(), bad, s))
         _lib.check(L.ifa_quantize_per_row(k.data_ptr(), rows, d, self.kc.data_ptr(),
                                           self.sk.data_ptr(), bad, s))
-        _lib.check(L.ifa_quantize_per_tensor(v.data_ptr(), self.slices, self.n, d,
-                                             self.vc.data_ptr(), self.sv.data_ptr(),
-                                             self.ws.data_ptr(), bad, s))
+        if self.v16 is not None:
+            _lib.check(L.ifa_quantize_per_tensor_v16(v.data_ptr(), self.slices, self.n, d,
+                                                     self.vc.data_ptr(), self.v16.data_ptr(),
+                                                     self.sv.data_ptr(), self.ws.data_ptr(),
+                                                     bad, s))
+        else:
+            _lib.check(L.ifa_quantize_per_tensor(v.data_ptr(), self.slices, self.n, d,
+                                                 self.vc.data_ptr(), self.sv.data_ptr(),
+                                                 self.ws.data_ptr(), bad, s))
 
     def attention(self, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
         s = int((stream or torch.cuda.current_stream(self.device)).cuda_stream)
+        if self.v16 is not None:
+            _lib.check(self.lib.ifa_int_flash_fwd_v16(
+                self.qc.data_ptr(), self.sq.data_ptr(), self.kc.data_ptr(), self.sk.data_ptr(),
+                self.vc.data_ptr(), self.v16.data_ptr(), self.sv.data_ptr(), self.out.data_ptr(),
+                self.slices, self.n, self.d, self.br, self.bc, self.flags, s))
+            return self.out
         _lib.check(self.lib.ifa_int_flash_fwd(
             self.qc.data_ptr(), self.sq.data_ptr(), self.kc.data_ptr(), self.sk.data_ptr(),
             self.vc.data_ptr(), self.sv.data_ptr(), self.out.data_ptr(), self.slices, self.n,
@@ -103,7 +120,9 @@ class AttentionPlan:
         fp16 conversion on the two-Q-tile path)."""
         elems = self.n * self.d
         v_fused = elems % 16 == 0 and self.d % 4 == 0
-        return 2 + (1 if v_fused else 3) + (2 if self.uses_pp_kernel() else 1)
+        pp = self.uses_pp_kernel()
+        conv = pp and (self.v16 is None or not v_fused)  # separate int8 -> fp16 pass
+        return 2 + (1 if v_fused else 3) + 1 + (1 if conv else 0)
 
     def check(self) -> None:
         """Raise like the reference if any quantized input was non-finite."""
