@@ -23,10 +23,11 @@
 // and P.V(j) reads it from there; the group waits for P.V(j-1) (which also
 // makes O(j-1) final) before it rescales O and overwrites P.
 //
-// Each thread writes its row's 32 keys (8k + 2t0 + e, k = 0..15) as 64
-// contiguous bytes, i.e. MMA keys [32 t0, 32 t0 + 32) in order 2k + e; the
-// fp16 V tile is loaded with its rows permuted the same way (smem row
-// 32t + 2k + e <- key 8k + 2t + e) by a 5-D tensor map.  Needs n % 128 == 0.
+// Each thread writes its row's 32 keys (8k + 2t0 + e, k = 0..15) as two
+// 32-byte runs, MMA keys 64h + 16 t0 + 2k' + e for k = 8h + k' (a layout
+// without shared-memory bank conflicts); the fp16 V tile is loaded with its
+// rows permuted the same way (smem row 64h + 16t + 2k' + e <- key 64h + 8k' +
+// 2t + e) by a 5-D tensor map.  Needs n % 128 == 0.
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         tma_load_3d(sm.k[ks], &tm_k, &sm.k_full[ks], 0, key0, slice, pol_keep);
                         if (i >= VST) bar_wait(b_v_empty + 8 * vs, vr.phase ^ 1u);
                         mbar_arrive_expect_tx(&sm.v_full[vs], BN * D * 2);
-                        const int32_t tile = (slice * n + key0) / BN;
+                        const int32_t tile = (slice * n + key0) / 64;  // 64-key halves
 #pragma unroll
                         for (int h = 0; h < D / 64; ++h)
                             tma_load_5d(sm.v[vs] + h * BN * 128, &tm_v, &sm.v_full[vs], 64 * h,
@@ -398,13 +399,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t bs_full = b_s_full + 8 * g, bs_empty = b_s_empty + 8 * g;
         const uint32_t bp_full = b_p_full + 8 * g, bp_empty = b_p_empty + 8 * g;
         const uint32_t bo_full = b_o_full + 8 * g, bo_free = b_o_free + 8 * g;
-        // P (fp16, K-major SW128): row r, MMA keys [32 t0, 32 t0 + 32) = 64 bytes =
-        // chunks 4 (t0 & 1) .. +3 of K-atom t0 >> 1, XOR-swizzled by r & 7.
+        // P (fp16, K-major SW128, two 64-key atoms): thread t0 of a row owns MMA
+        // keys [16 t0, 16 t0 + 16) of each atom = 16-byte chunks 2 t0, 2 t0 + 1,
+        // XOR-swizzled by r & 7.  The eight lanes of a quarter warp (two rows x
+        // four t0) then hit eight different bank groups: no store conflicts.
         uint32_t p_row[2];
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             const uint32_t row = static_cast<uint32_t>(row0) + 8 * r;
-            p_row[r] = smem_u32(sm.p[g]) + (t0 >> 1) * (BM * 128) + row * 128;
+            p_row[r] = smem_u32(sm.p[g]) + row * 128;
         }
         const uint32_t sw = static_cast<uint32_t>(row0) & 7;  // same for row0 + 8
         Ring<KST> kv;
@@ -548,9 +551,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int r = 0; r < 2; ++r)
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        const uint32_t chunk = (4 * (t0 & 1) + i) ^ sw;
+                        // words 4i..4i+3 = pairs k = 4i..4i+3: atom i >> 1, chunk 2 t0 + (i & 1)
+                        const uint32_t chunk = (2 * t0 + (i & 1)) ^ sw;
                         asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
-                                         p_row[r] + chunk * 16),
+                                         p_row[r] + (i >> 1) * (BM * 128) + chunk * 16),
                                      "r"(wd[r][4 * i]), "r"(wd[r][4 * i + 1]),
                                      "r"(wd[r][4 * i + 2]), "r"(wd[r][4 * i + 3])
                                      : "memory");
@@ -673,18 +677,18 @@ static bool make_map_codes(CUtensorMap* map, const int8_t* base, int64_t slices,
            CUDA_SUCCESS;
 }
 
-// fp16 V [slices*n][D] viewed as {64 cols, e:2, k:16, t:4, tile} so that
-// smem row 32t + 2k + e of a 128-key tile holds key 8k + 2t + e: the MMA key
-// order of the P rows the softmax threads write (thread t0 of a row owns MMA
-// keys [32 t0, 32 t0 + 32) = its keys 8k + 2 t0 + e).
+// fp16 V [slices*n][D] viewed as {64 cols, e:2, k':8, t:4, half} so that
+// smem row 64h + 16t + 2k' + e holds key 64h + 8k' + 2t + e: the MMA key
+// order of the P rows the softmax threads write (thread t0 owns MMA keys
+// 64h + 16 t0 + 2k' + e = its keys 8(8h + k') + 2 t0 + e).
 static bool make_map_v16(CUtensorMap* map, const __half* base, int64_t slices, int64_t n, int D) {
     PFN_encodeTiled enc = get_encode();
     if (!enc || n % 128 != 0) return false;
     const cuuint64_t row = static_cast<cuuint64_t>(D) * 2;
-    const cuuint64_t dims[5] = {static_cast<cuuint64_t>(D), 2, 16, 4,
-                                static_cast<cuuint64_t>(slices * n / 128)};
-    const cuuint64_t strides[4] = {row, 8 * row, 2 * row, 128 * row};
-    const cuuint32_t box[5] = {64u, 2u, 16u, 4u, 1u};
+    const cuuint64_t dims[5] = {static_cast<cuuint64_t>(D), 2, 8, 4,
+                                static_cast<cuuint64_t>(slices * n / 64)};
+    const cuuint64_t strides[4] = {row, 8 * row, 2 * row, 64 * row};
+    const cuuint32_t box[5] = {64u, 2u, 8u, 4u, 2u};
     const cuuint32_t estr[5] = {1u, 1u, 1u, 1u, 1u};
     return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, const_cast<__half*>(base), dims, strides,
                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
