@@ -34,6 +34,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "ifa_internal.h"
 #include "ptx.cuh"
@@ -468,104 +469,114 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
                 __syncwarp();
                 if (lane == 0) bar_arrive(b_k_empty + 8 * st);
-                const bool dmask = j == diag;  // keys > row inside the diagonal tile
-                if (dmask) {
-#pragma unroll
-                    for (int k = 0; k < 16; ++k)
-#pragma unroll
-                        for (int r = 0; r < 2; ++r)
-#pragma unroll
-                            for (int e = 0; e < 2; ++e)
-                                if (8 * k + 2 * static_cast<int32_t>(t0) + e > row0 + 8 * r)
-                                    u[4 * k + 2 * r + e] = -__int_as_float(0x7f800000);
-                }
-                float cr[2], alpha[2];
-#pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    float a[11];
-#pragma unroll
-                    for (int jj = 0; jj < 10; ++jj) {
-                        const int v0 = 3 * jj, v1 = 3 * jj + 1, v2 = 3 * jj + 2;
-                        a[jj] = fmax3(u[4 * (v0 >> 1) + 2 * r + (v0 & 1)],
-                                      u[4 * (v1 >> 1) + 2 * r + (v1 & 1)],
-                                      u[4 * (v2 >> 1) + 2 * r + (v2 & 1)]);
+                // rest of the tile, instantiated twice so the diagonal masking of
+                // the causal kernel never becomes per-element predicated code on the
+                // other tiles
+                auto rest = [&](auto diag_tag) {
+                    constexpr bool dmask = decltype(diag_tag)::value;  // keys > row masked
+                    if (dmask) {
+    #pragma unroll
+                        for (int k = 0; k < 16; ++k)
+    #pragma unroll
+                            for (int r = 0; r < 2; ++r)
+    #pragma unroll
+                                for (int e = 0; e < 2; ++e)
+                                    if (8 * k + 2 * static_cast<int32_t>(t0) + e > row0 + 8 * r)
+                                        u[4 * k + 2 * r + e] = -__int_as_float(0x7f800000);
                     }
-                    a[10] = fmaxf(u[4 * 15 + 2 * r], u[4 * 15 + 2 * r + 1]);
-                    float b = fmaxf(fmax3(fmax3(a[0], a[1], a[2]), fmax3(a[3], a[4], a[5]),
-                                          fmax3(a[6], a[7], a[8])),
-                                    fmaxf(a[9], a[10]));
-                    b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, 1));
-                    b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, 2));
-                    const float mnew = (m[r] < b) ? b : m[r];
-                    cr[r] = kLog2_127 - sq[r] * mnew;
-                    alpha[r] = (j == 0 || mnew == m[r]) ? 1.0f : ex2(sq[r] * (m[r] - mnew));
-                    m[r] = mnew;
-                }
-                // codes: round(2^t) as exact fp16 integers; 6 of 8 exp2 on MUFU,
-                // 2 on the FMA pipe.  wd[r][k] = keys (8k + 2t0, +1) of row r.
-                uint32_t wd[2][16];
-                float2 ls[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-#pragma unroll
+                    float cr[2], alpha[2];
+    #pragma unroll
                     for (int r = 0; r < 2; ++r) {
-                        const float2 t = ffma2(make_float2(u[4 * k + 2 * r], u[4 * k + 2 * r + 1]),
-                                               f2(sq[r]), f2(cr[r]));
-                        const float2 y = (k & kPolyMask) == kPolyMask ? exp2_poly2(t)
-                                                      : make_float2(ex2(t.x), ex2(t.y));
-                        float2 c = fsub2(fadd2(y, f2(kMagic)), f2(kMagic));
-                        if (dmask) {  // masked keys weigh 0 (also when sQ == 0)
-                            const int32_t key = 8 * k + 2 * static_cast<int32_t>(t0);
-                            if (key > row0 + 8 * r) c.x = 0.0f;
-                            if (key + 1 > row0 + 8 * r) c.y = 0.0f;
+                        float a[11];
+    #pragma unroll
+                        for (int jj = 0; jj < 10; ++jj) {
+                            const int v0 = 3 * jj, v1 = 3 * jj + 1, v2 = 3 * jj + 2;
+                            a[jj] = fmax3(u[4 * (v0 >> 1) + 2 * r + (v0 & 1)],
+                                          u[4 * (v1 >> 1) + 2 * r + (v1 & 1)],
+                                          u[4 * (v2 >> 1) + 2 * r + (v2 & 1)]);
                         }
-                        ls[r] = fadd2(ls[r], c);
-                        const __half2 h = __floats2half2_rn(c.x, c.y);
-                        wd[r][k] = *reinterpret_cast<const uint32_t*>(&h);
+                        a[10] = fmaxf(u[4 * 15 + 2 * r], u[4 * 15 + 2 * r + 1]);
+                        float b = fmaxf(fmax3(fmax3(a[0], a[1], a[2]), fmax3(a[3], a[4], a[5]),
+                                              fmax3(a[6], a[7], a[8])),
+                                        fmaxf(a[9], a[10]));
+                        b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, 1));
+                        b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, 2));
+                        const float mnew = (m[r] < b) ? b : m[r];
+                        cr[r] = kLog2_127 - sq[r] * mnew;
+                        alpha[r] = (j == 0 || mnew == m[r]) ? 1.0f : ex2(sq[r] * (m[r] - mnew));
+                        m[r] = mnew;
                     }
-                }
-                // P.V(j-1) done: the P buffer is free and O(j-1) is final
-                if (tc > 0) bar_wait(bp_empty, (tc - 1) & 1);
-                tc_fence_after();
-                const bool need = j > 0 && (alpha[0] != 1.0f || alpha[1] != 1.0f);
-                if (__any_sync(0xffffffffu, need)) {
-#pragma unroll
-                    for (int c = 0; c < D / 32; ++c) {
-                        uint32_t o[16];
-                        ld16x256_x4(t_o + 32 * c, o);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int k = 0; k < 4; ++k)
-#pragma unroll
-                            for (int r = 0; r < 2; ++r) {
-                                const float2 v = fmul2(make_float2(__uint_as_float(o[4 * k + 2 * r]),
-                                                                   __uint_as_float(o[4 * k + 2 * r + 1])),
-                                                       f2(alpha[r]));
-                                o[4 * k + 2 * r] = __float_as_uint(v.x);
-                                o[4 * k + 2 * r + 1] = __float_as_uint(v.y);
+                    // codes: round(2^t) as exact fp16 integers; 6 of 8 exp2 on MUFU,
+                    // 2 on the FMA pipe.  wd[r][k] = keys (8k + 2t0, +1) of row r.
+                    uint32_t wd[2][16];
+                    float2 ls[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
+    #pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+    #pragma unroll
+                        for (int r = 0; r < 2; ++r) {
+                            const float2 t = ffma2(make_float2(u[4 * k + 2 * r], u[4 * k + 2 * r + 1]),
+                                                   f2(sq[r]), f2(cr[r]));
+                            const float2 y = (k & kPolyMask) == kPolyMask ? exp2_poly2(t)
+                                                          : make_float2(ex2(t.x), ex2(t.y));
+                            float2 c = fsub2(fadd2(y, f2(kMagic)), f2(kMagic));
+                            if (dmask) {  // masked keys weigh 0 (also when sQ == 0)
+                                const int32_t key = 8 * k + 2 * static_cast<int32_t>(t0);
+                                if (key > row0 + 8 * r) c.x = 0.0f;
+                                if (key + 1 > row0 + 8 * r) c.y = 0.0f;
                             }
-                        st16x256_x4(t_o + 32 * c, o);
+                            ls[r] = fadd2(ls[r], c);
+                            const __half2 h = __floats2half2_rn(c.x, c.y);
+                            wd[r][k] = *reinterpret_cast<const uint32_t*>(&h);
+                        }
                     }
-                    tmem_wait_st();
-                }
-#pragma unroll
-                for (int r = 0; r < 2; ++r)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        // words 4i..4i+3 = pairs k = 4i..4i+3: atom i >> 1, chunk 2 t0 + (i & 1)
-                        const uint32_t chunk = (2 * t0 + (i & 1)) ^ sw;
-                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
-                                         p_row[r] + (i >> 1) * (BM * 128) + chunk * 16),
-                                     "r"(wd[r][4 * i]), "r"(wd[r][4 * i + 1]),
-                                     "r"(wd[r][4 * i + 2]), "r"(wd[r][4 * i + 3])
-                                     : "memory");
+                    // P.V(j-1) done: the P buffer is free and O(j-1) is final
+                    if (tc > 0) bar_wait(bp_empty, (tc - 1) & 1);
+                    tc_fence_after();
+                    const bool need = j > 0 && (alpha[0] != 1.0f || alpha[1] != 1.0f);
+                    if (__any_sync(0xffffffffu, need)) {
+    #pragma unroll
+                        for (int c = 0; c < D / 32; ++c) {
+                            uint32_t o[16];
+                            ld16x256_x4(t_o + 32 * c, o);
+                            tmem_wait_ld();
+    #pragma unroll
+                            for (int k = 0; k < 4; ++k)
+    #pragma unroll
+                                for (int r = 0; r < 2; ++r) {
+                                    const float2 v = fmul2(make_float2(__uint_as_float(o[4 * k + 2 * r]),
+                                                                       __uint_as_float(o[4 * k + 2 * r + 1])),
+                                                           f2(alpha[r]));
+                                    o[4 * k + 2 * r] = __float_as_uint(v.x);
+                                    o[4 * k + 2 * r + 1] = __float_as_uint(v.y);
+                                }
+                            st16x256_x4(t_o + 32 * c, o);
+                        }
+                        tmem_wait_st();
                     }
-                fence_proxy_async_shared();  // P is read by the tensor core
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) bar_arrive(bp_full);
+    #pragma unroll
+                    for (int r = 0; r < 2; ++r)
+    #pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            // words 4i..4i+3 = pairs k = 4i..4i+3: atom i >> 1, chunk 2 t0 + (i & 1)
+                            const uint32_t chunk = (2 * t0 + (i & 1)) ^ sw;
+                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                             p_row[r] + (i >> 1) * (BM * 128) + chunk * 16),
+                                         "r"(wd[r][4 * i]), "r"(wd[r][4 * i + 1]),
+                                         "r"(wd[r][4 * i + 2]), "r"(wd[r][4 * i + 3])
+                                         : "memory");
+                        }
+                    fence_proxy_async_shared();  // P is read by the tensor core
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) bar_arrive(bp_full);
+
 #pragma unroll
-                for (int r = 0; r < 2; ++r) l[r] = __fmaf_rn(l[r], alpha[r], ls[r].x + ls[r].y);
+                    for (int r = 0; r < 2; ++r) l[r] = __fmaf_rn(l[r], alpha[r], ls[r].x + ls[r].y);
+                };
+                if (causal && j == diag)
+                    rest(std::true_type{});
+                else
+                    rest(std::false_type{});
                 kv.advance();
                 ++tc;
             }
@@ -782,12 +793,6 @@ bool int_flash_pp_eligible(const AttnArgs& a) {
     if (off && off[0] == '1') return false;
     const int64_t bc = a.bc < a.n ? a.bc : a.n;
     const bool tiles_are_blocks = bc == pp::BN || (bc == a.n && a.n <= pp::BN);
-    // causal: correct (tests), but on C3 the pair-ordered LPT schedule keeps
-    // all slices' K and fp16 V (192 MB) in flight and loses to the quad
-    // kernel (2.71 vs 2.55 ms), so it is opt-in
-    const char* pc = std::getenv("IFA_B200_PP_CAUSAL");
-    const bool causal_ok = pc && pc[0] == '1';
-    if ((a.flags & IFA_FLAG_CAUSAL) && !causal_ok) return false;
     return (a.flags & IFA_FLAG_FAST) &&
            a.audit == nullptr && tiles_are_blocks && a.n % 128 == 0 && a.d <= 128;
 }

@@ -102,13 +102,10 @@ class AttentionPlan:
 
     def uses_pp_kernel(self) -> bool:
         """True when ifa_int_flash_fwd takes the two-Q-tile tolerance kernel
-        (csrc/attn_pp.cu: fast mode, Bc = 128, n % 128 == 0; causal only with
-        IFA_B200_PP_CAUSAL=1),
+        (csrc/attn_pp.cu: fast mode, Bc = 128, n % 128 == 0),
         which first converts the V codes to fp16 (one extra launch)."""
         bc = min(self.bc, self.n)
         blocks = bc == 128 or (bc == self.n and self.n <= 128)
-        if (self.flags & _lib.FLAG_CAUSAL) and os.environ.get("IFA_B200_PP_CAUSAL", "") != "1":
-            return False
         return bool(self.flags & _lib.FLAG_FAST) and \
             blocks and self.n % 128 == 0 and self.d <= 128 and \
             os.environ.get("IFA_B200_NO_PP", "") != "1"

@@ -323,7 +323,6 @@ def test_fast_mode_pp_kernel(ifa, oracle, dist, n, d, sqrt_d, causal, monkeypatc
     (IFA_B200_NO_PP=1) far inside it.  n = 384 has an odd number of Q tiles
     (the second tile of the last pair is all padding); causal pairs give the
     two groups different KV tile counts."""
-    monkeypatch.setenv("IFA_B200_PP_CAUSAL", "1")  # causal is opt-in on this kernel
     _, (qc, qs, kc, ks, vc, vs) = _quantized_case(oracle, dist, n, d, seed=3 * n + d)
     want = oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, 128,
                                       flags=(1 if sqrt_d else 0) | (2 if causal else 0))
