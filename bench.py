@@ -518,10 +518,13 @@ def main() -> None:
         }
         hbm = load_peaks().get("hbm_gbs") or 6650.0
         qbytes = 3 * slices * N * d * 5 + 2 * slices * N * 4 + slices * 4
+        if plan.v16 is not None:  # fp16 V codes written alongside the int8 ones
+            qbytes += slices * N * d * 2
         line["quantize_roofline"] = {
             "bound": "hbm", "achieved": qbytes / quant_s / 1e9, "peak": hbm, "unit": "GB/s",
             "frac": qbytes / quant_s / 1e9 / hbm, "algorithmic_bytes": qbytes,
-            "note": "V: per-slice cluster kernel, second pass re-reads the slice from L2"}
+            "note": "V: per-slice cluster kernel, second pass re-reads the slice from L2"
+                    + ("; also writes the fp16 V codes" if plan.v16 is not None else "")}
         # the other mode on the same inputs: exact (bitwise) vs tolerance
         other = "exact" if args.mode == "fast" else "fast"
         try:
