@@ -178,7 +178,9 @@ def half_int8_timing(torch, plan, v, slices, n, d, ops, stream, steps) -> dict:
         e1.synchronize()
         res[name] = e0.elapsed_time(e1) / steps
     res["attention_tops"] = ops / (res["attention_ms"] / 1e3) / 1e12
-    res["kernel"] = "half_int8_fwd_kernel (int8 S, fp16 P.V, f32 accumulate)"
+    res["kernel"] = ("int_flash_pp_kernel<MODE=half> (int8 S, fp16 P.V into f32 TMEM)"
+                     if n % 128 == 0 and d in (64, 128) else
+                     "half_int8_fwd_kernel (int8 S, fp16 P.V, f32 accumulate)")
     return res
 
 
@@ -221,7 +223,9 @@ def fp8_timing(torch, q, k, v, slices, n, d, ops, stream, steps) -> dict:
         e1.synchronize()
         res[name] = e0.elapsed_time(e1) / steps
     res["attention_tops"] = ops / (res["attention_ms"] / 1e3) / 1e12
-    res["kernel"] = "half_int8_fwd_kernel<D, FP8> (e4m3 S on kind::f8f6f4, fp16 P.V)"
+    res["kernel"] = ("int_flash_pp_kernel<MODE=fp8> (e4m3 S on kind::f8f6f4, fp16 P.V into f32 TMEM)"
+                     if n % 128 == 0 and d in (64, 128) else
+                     "half_int8_fwd_kernel<D, FP8> (e4m3 S on kind::f8f6f4, fp16 P.V)")
     return res
 
 

@@ -249,9 +249,13 @@ int ifa_half_int8_fwd(const int8_t* q, const float* sq, const int8_t* k, const f
     if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) |
          reinterpret_cast<uintptr_t>(v_f16)) % 16 != 0)
         return fail(IFA_EINVAL, "half_int8_attention: q/k/v must be 16-byte aligned");
-    const cudaError_t e = ifa_b200::launch_half_int8_fwd(
-        q, sq, k, sk, v_f16, o, slices, n, d, d, (flags & IFA_FLAG_SQRT_D) != 0,
-        static_cast<cudaStream_t>(stream));
+    const cudaError_t e =
+        ifa_b200::float_weights_pp_eligible(n, d)
+            ? ifa_b200::launch_half_int8_pp(q, sq, k, sk, v_f16, o, slices, n, d, flags,
+                                            static_cast<cudaStream_t>(stream))
+            : ifa_b200::launch_half_int8_fwd(q, sq, k, sk, v_f16, o, slices, n, d, d,
+                                             (flags & IFA_FLAG_SQRT_D) != 0,
+                                             static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? IFA_OK : cuda_fail(e, "half_int8_attention");
 }
 
@@ -301,9 +305,13 @@ int ifa_fp8_attention_fwd(const uint8_t* q, const float* q_scales, const uint8_t
     if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) |
          reinterpret_cast<uintptr_t>(v_f16)) % 16 != 0)
         return fail(IFA_EINVAL, "fp8_emulated_attention: q/k/v must be 16-byte aligned");
-    const cudaError_t e = ifa_b200::launch_fp8_attention_fwd(
-        q, q_scales, k, k_scales, v_f16, v_scales, o, slices, n, d,
-        (flags & IFA_FLAG_SQRT_D) != 0, static_cast<cudaStream_t>(stream));
+    const cudaError_t e =
+        ifa_b200::float_weights_pp_eligible(n, d)
+            ? ifa_b200::launch_fp8_pp(q, q_scales, k, k_scales, v_f16, v_scales, o, slices, n, d,
+                                      flags, static_cast<cudaStream_t>(stream))
+            : ifa_b200::launch_fp8_attention_fwd(q, q_scales, k, k_scales, v_f16, v_scales, o,
+                                                 slices, n, d, (flags & IFA_FLAG_SQRT_D) != 0,
+                                                 static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? IFA_OK : cuda_fail(e, "fp8_emulated_attention");
 }
 

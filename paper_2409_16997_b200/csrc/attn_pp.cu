@@ -196,14 +196,36 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uin
         : "memory");
 }
 
-template <int D, bool CAUSAL>
+// MODE: what the weights and S are (the pipeline is the same).
+//   kModeCodes (0): full-INT8 tolerance mode -- int8 S (kind::i8), P = the
+//                   integer codes round(127 exp(s - m)), O * sV / l.
+//   kModeHalf  (1): half-INT8 (attention.cpp:359-399) -- int8 S, float
+//                   weights exp(s - m) as fp16, V = fp16 of the float V, O / l.
+//   kModeFp8   (2): fp8_emulated_attention (attention.cpp:401-407) -- e4m3 S
+//                   (kind::f8f6f4), one scale per slice, V = decoded e4m3,
+//                   O / (l sV).
+constexpr int kModeCodes = 0, kModeHalf = 1, kModeFp8 = 2;
+
+__device__ __forceinline__ void mma_f8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+template <int D, bool CAUSAL, int MODE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     int_flash_pp_kernel(const __grid_constant__ CUtensorMap tm_q,
                         const __grid_constant__ CUtensorMap tm_k,
                         const __grid_constant__ CUtensorMap tm_v, const Params p) {
     constexpr uint32_t kLayout = D == 128 ? kLayoutSw128 : kLayoutSw64;
     constexpr uint32_t kSbo = 8 * D;
-    constexpr uint32_t kIdescS = idesc_i8(BM, BN, false, false);
+    constexpr uint32_t kIdescS = MODE == kModeFp8
+                                     ? ((1u << 4) | ((BN >> 3) << 17) | ((BM >> 4) << 24))
+                                     : idesc_i8(BM, BN, false, false);
     constexpr uint32_t kIdescPV = idesc_f16(BM, D, true);
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -278,11 +300,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int32_t key0 = 0; key0 < w.jt * BN; key0 += BN) {
                     const uint32_t ks = kr.idx, vs = vr.idx;
                     if (i >= KST) bar_wait(b_k_empty + 8 * ks, kr.phase ^ 1u);
-                    float4 k4 = __ldg(reinterpret_cast<const float4*>(sk_slice + key0) + lane);
-                    k4.x *= p.sk_mul;
-                    k4.y *= p.sk_mul;
-                    k4.z *= p.sk_mul;
-                    k4.w *= p.sk_mul;
+                    float4 k4;
+                    if constexpr (MODE == kModeFp8) {  // s = S / (sQ sK): one constant per slice
+                        const float c8 = __fdiv_rn(p.sk_mul, __fmul_rn(p.sq[slice], p.sk[slice]));
+                        k4 = make_float4(c8, c8, c8, c8);
+                    } else {
+                        k4 = __ldg(reinterpret_cast<const float4*>(sk_slice + key0) + lane);
+                        k4.x *= p.sk_mul;
+                        k4.y *= p.sk_mul;
+                        k4.z *= p.sk_mul;
+                        k4.w *= p.sk_mul;
+                    }
                     reinterpret_cast<float4*>(sm.sk[ks])[lane] = k4;
                     if (lane == 0) {
                         mbar_arrive_expect_tx(&sm.k_full[ks], BN * D);
@@ -323,7 +351,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     for (int kk = 0; kk < D / 32; ++kk) {
                         const uint64_t adesc = smem_desc(q_base + kk * 32, 16, kSbo, kLayout);
                         const uint64_t bdesc = smem_desc(k_base + kk * 32, 16, kSbo, kLayout);
-                        mma_i8_ss(d_s, adesc, bdesc, kIdescS, kk > 0 ? 1u : 0u);
+                        if constexpr (MODE == kModeFp8)
+                            mma_f8_ss(d_s, adesc, bdesc, kIdescS, kk > 0 ? 1u : 0u);
+                        else
+                            mma_i8_ss(d_s, adesc, bdesc, kIdescS, kk > 0 ? 1u : 0u);
                     }
                     mma_commit_u32(b_s_full + 8 * g);
                 };
@@ -426,7 +457,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 grow[r] = q0 + row0 + 8 * r;
-                sq[r] = grow[r] < n ? p.sq[static_cast<int64_t>(slice) * n + grow[r]] : 0.0f;
+                if constexpr (MODE == kModeFp8)
+                    sq[r] = 1.0f;  // the scales are in the per-key constant
+                else
+                    sq[r] = grow[r] < n ? p.sq[static_cast<int64_t>(slice) * n + grow[r]] : 0.0f;
             }
             float l[2] = {0.0f, 0.0f}, m[2] = {-__int_as_float(0x7f800000), -__int_as_float(0x7f800000)};
 
@@ -456,12 +490,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int k = 0; k < 16; ++k) {
                     const float2 s2 = *reinterpret_cast<const float2*>(skc + 8 * k);
-                    const float2 a = fmul2(make_float2(__int2float_rn(static_cast<int32_t>(sr[4 * k])),
-                                                       __int2float_rn(static_cast<int32_t>(sr[4 * k + 1]))),
-                                           s2);
-                    const float2 b = fmul2(make_float2(__int2float_rn(static_cast<int32_t>(sr[4 * k + 2])),
-                                                       __int2float_rn(static_cast<int32_t>(sr[4 * k + 3]))),
-                                           s2);
+                    float2 fa, fb;  // S as f32: exact int32 (kind::i8) or f32 (kind::f8f6f4)
+                    if constexpr (MODE == kModeFp8) {
+                        fa = make_float2(__uint_as_float(sr[4 * k]), __uint_as_float(sr[4 * k + 1]));
+                        fb = make_float2(__uint_as_float(sr[4 * k + 2]), __uint_as_float(sr[4 * k + 3]));
+                    } else {
+                        fa = make_float2(__int2float_rn(static_cast<int32_t>(sr[4 * k])),
+                                         __int2float_rn(static_cast<int32_t>(sr[4 * k + 1])));
+                        fb = make_float2(__int2float_rn(static_cast<int32_t>(sr[4 * k + 2])),
+                                         __int2float_rn(static_cast<int32_t>(sr[4 * k + 3])));
+                    }
+                    const float2 a = fmul2(fa, s2);
+                    const float2 b = fmul2(fb, s2);
                     u[4 * k] = a.x;
                     u[4 * k + 1] = a.y;
                     u[4 * k + 2] = b.x;
@@ -502,7 +542,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, 1));
                         b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, 2));
                         const float mnew = (m[r] < b) ? b : m[r];
-                        cr[r] = kLog2_127 - sq[r] * mnew;
+                        cr[r] = (MODE == kModeCodes ? kLog2_127 : 0.0f) - sq[r] * mnew;
                         alpha[r] = (j == 0 || mnew == m[r]) ? 1.0f : ex2(sq[r] * (m[r] - mnew));
                         m[r] = mnew;
                     }
@@ -518,7 +558,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                                    f2(sq[r]), f2(cr[r]));
                             const float2 y = (k & kPolyMask) == kPolyMask ? exp2_poly2(t)
                                                           : make_float2(ex2(t.x), ex2(t.y));
-                            float2 c = fsub2(fadd2(y, f2(kMagic)), f2(kMagic));
+                            // full-INT8: the integer code; half-INT8 / FP8: the float weight
+                            float2 c = MODE == kModeCodes ? fsub2(fadd2(y, f2(kMagic)), f2(kMagic)) : y;
                             if (dmask) {  // masked keys weigh 0 (also when sQ == 0)
                                 const int32_t key = 8 * k + 2 * static_cast<int32_t>(t0);
                                 if (key > row0 + 8 * r) c.x = 0.0f;
@@ -581,14 +622,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 ++tc;
             }
             // epilogue: O * sV / l, l summed over the quad
-            const float sv = p.sv[slice];
             float f[2];
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 float lt = l[r];
                 lt += __shfl_xor_sync(0xffffffffu, lt, 1);
                 lt += __shfl_xor_sync(0xffffffffu, lt, 2);
-                f[r] = __fdiv_rn(sv, lt);
+                if constexpr (MODE == kModeCodes)
+                    f[r] = __fdiv_rn(p.sv[slice], lt);
+                else if constexpr (MODE == kModeHalf)
+                    f[r] = __fdiv_rn(1.0f, lt);  // finalize_softmax_state (attention.cpp:139-149)
+                else
+                    f[r] = __fdiv_rn(__fdiv_rn(1.0f, lt), p.sv[slice]);  // V = decode / sV
             }
             bar_wait(bo_full, wi & 1);
             tc_fence_after();
@@ -708,6 +753,60 @@ static bool make_map_v16(CUtensorMap* map, const __half* base, int64_t slices, i
            CUDA_SUCCESS;
 }
 
+template <int D, int MODE>
+static cudaError_t run(const void* q, const void* k, const __half* v16, const Params& p,
+                       int64_t pitch, bool causal, cudaStream_t stream) {
+    CUtensorMap tq, tk, tv;
+    if (!make_map_codes(&tq, static_cast<const int8_t*>(q), p.slices, p.n, pitch, D) ||
+        !make_map_codes(&tk, static_cast<const int8_t*>(k), p.slices, p.n, pitch, D) ||
+        !make_map_v16(&tv, v16, p.slices, p.n, D))
+        return cudaErrorInvalidValue;
+    const size_t smem = sizeof(Smem<D>) + 1024;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(int_flash_pp_kernel<D, false, MODE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e == cudaSuccess && MODE == kModeCodes)
+            e = cudaFuncSetAttribute(int_flash_pp_kernel<D, true, MODE>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    const int grid = p.items < sms ? p.items : sms;
+    if (MODE == kModeCodes && causal)
+        int_flash_pp_kernel<D, true, MODE><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+    else
+        int_flash_pp_kernel<D, false, MODE><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+    return cudaGetLastError();
+}
+
+static Params make_params(const float* sq, const float* sk, const float* sv, float* o,
+                          int64_t slices, int64_t n, int64_t d, uint32_t flags) {
+    Params p;
+    p.sq = sq;
+    p.sk = sk;
+    p.sv = sv;
+    p.o = o;
+    p.n = static_cast<int32_t>(n);
+    p.d = static_cast<int32_t>(d);
+    p.flags = flags;
+    p.sk_mul = kLog2e * ((flags & IFA_FLAG_SQRT_D) ? 1.0f / sqrtf(static_cast<float>(d)) : 1.0f);
+    const int32_t q_tiles = static_cast<int32_t>((n + BM - 1) / BM);
+    p.pairs = (q_tiles + 1) / 2;
+    p.slices = static_cast<int32_t>(slices);
+    p.items = p.pairs * p.slices;
+    return p;
+}
+
 template <int D>
 static cudaError_t launch(const AttnArgs& a, const uint16_t* v16_given, cudaStream_t stream) {
     static bool pool_kept = false;
@@ -733,55 +832,8 @@ static cudaError_t launch(const AttnArgs& a, const uint16_t* v16_given, cudaStre
         codes_to_f16_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(a.v, rows, a.pitch,
                                                                                 D, v16);
     }
-    CUtensorMap tq, tk, tv;
-    if (!make_map_codes(&tq, a.q, a.slices, a.n, a.pitch, D) ||
-        !make_map_codes(&tk, a.k, a.slices, a.n, a.pitch, D) ||
-        !make_map_v16(&tv, v16, a.slices, a.n, D)) {
-        if (owned) cudaFreeAsync(owned, stream);
-        return cudaErrorInvalidValue;
-    }
-    Params p;
-    p.sq = a.sq;
-    p.sk = a.sk;
-    p.sv = a.sv;
-    p.o = a.o;
-    p.n = static_cast<int32_t>(a.n);
-    p.d = static_cast<int32_t>(a.d);
-    p.flags = a.flags;
-    p.sk_mul = kLog2e * ((a.flags & IFA_FLAG_SQRT_D) ? 1.0f / sqrtf(static_cast<float>(a.d)) : 1.0f);
-    const int32_t q_tiles = static_cast<int32_t>((a.n + BM - 1) / BM);
-    p.pairs = (q_tiles + 1) / 2;
-    p.slices = static_cast<int32_t>(a.slices);
-    p.items = p.pairs * p.slices;
-    const size_t smem = sizeof(Smem<D>) + 1024;
-    static bool configured = false;
-    if (!configured) {
-        e = cudaFuncSetAttribute(int_flash_pp_kernel<D, false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem));
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(int_flash_pp_kernel<D, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem));
-        if (e != cudaSuccess) {
-            if (owned) cudaFreeAsync(owned, stream);
-            return e;
-        }
-        configured = true;
-    }
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    const int grid = p.items < sms ? p.items : sms;
-    if (a.flags & IFA_FLAG_CAUSAL)
-        int_flash_pp_kernel<D, true><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
-    else
-        int_flash_pp_kernel<D, false><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
-    e = cudaGetLastError();
+    const Params p = make_params(a.sq, a.sk, a.sv, a.o, a.slices, a.n, a.d, a.flags);
+    e = run<D, kModeCodes>(a.q, a.k, v16, p, a.pitch, (a.flags & IFA_FLAG_CAUSAL) != 0, stream);
     const cudaError_t e2 = owned ? cudaFreeAsync(owned, stream) : cudaSuccess;
     return e != cudaSuccess ? e : e2;
 }
@@ -800,6 +852,32 @@ bool int_flash_pp_eligible(const AttnArgs& a) {
 cudaError_t launch_int_flash_pp(const AttnArgs& a, const uint16_t* v16, cudaStream_t stream) {
     if (a.d <= 64) return pp::launch<64>(a, v16, stream);
     return pp::launch<128>(a, v16, stream);
+}
+
+bool float_weights_pp_eligible(int64_t n, int64_t d) {
+    const char* off = std::getenv("IFA_B200_NO_PP");
+    if (off && off[0] == '1') return false;
+    return n % 128 == 0 && (d == 64 || d == 128);
+}
+
+cudaError_t launch_half_int8_pp(const int8_t* q, const float* sq, const int8_t* k,
+                                const float* sk, const uint16_t* v16, float* o, int64_t slices,
+                                int64_t n, int64_t d, uint32_t flags, cudaStream_t stream) {
+    const pp::Params p = pp::make_params(sq, sk, nullptr, o, slices, n, d, flags & IFA_FLAG_SQRT_D);
+    const __half* vh = reinterpret_cast<const __half*>(v16);
+    if (d == 64) return pp::run<64, pp::kModeHalf>(q, k, vh, p, d, false, stream);
+    return pp::run<128, pp::kModeHalf>(q, k, vh, p, d, false, stream);
+}
+
+cudaError_t launch_fp8_pp(const uint8_t* q, const float* q_scales, const uint8_t* k,
+                          const float* k_scales, const uint16_t* v16, const float* v_scales,
+                          float* o, int64_t slices, int64_t n, int64_t d, uint32_t flags,
+                          cudaStream_t stream) {
+    const pp::Params p = pp::make_params(q_scales, k_scales, v_scales, o, slices, n, d,
+                                         flags & IFA_FLAG_SQRT_D);
+    const __half* vh = reinterpret_cast<const __half*>(v16);
+    if (d == 64) return pp::run<64, pp::kModeFp8>(q, k, vh, p, d, false, stream);
+    return pp::run<128, pp::kModeFp8>(q, k, vh, p, d, false, stream);
 }
 
 }  // namespace ifa_b200

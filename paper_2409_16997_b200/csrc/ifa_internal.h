@@ -51,6 +51,16 @@ bool int_flash_pp_eligible(const AttnArgs& a);
 // v16: [slices][n][D] fp16 copy of the V codes (D = 64 for d <= 64, else
 // 128), or null to convert a.v internally.
 cudaError_t launch_int_flash_pp(const AttnArgs& a, const uint16_t* v16, cudaStream_t stream);
+// The same two-Q-tile pipeline for the float-weight variants (§8(f) f1, f3):
+// n % 128 == 0, d in {64, 128}, non-causal; v16 = fp16 V [slices][n][d].
+bool float_weights_pp_eligible(int64_t n, int64_t d);
+cudaError_t launch_half_int8_pp(const int8_t* q, const float* sq, const int8_t* k,
+                                const float* sk, const uint16_t* v16, float* o, int64_t slices,
+                                int64_t n, int64_t d, uint32_t flags, cudaStream_t stream);
+cudaError_t launch_fp8_pp(const uint8_t* q, const float* q_scales, const uint8_t* k,
+                          const float* k_scales, const uint16_t* v16, const float* v_scales,
+                          float* o, int64_t slices, int64_t n, int64_t d, uint32_t flags,
+                          cudaStream_t stream);
 
 // attn_half.cu: half-INT8 forward (q/k codes of row pitch `pitch`, v fp16
 // [slices][n][d] dense, d in {64, 128}) and the f32 -> fp16 conversion.
