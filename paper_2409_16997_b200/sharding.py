@@ -4,7 +4,7 @@ Every (b,h) slice is an independent attention problem (the reference's
 harness loops them, eval.cpp:167-168; V's tensor scale is per slice,
 eval.cpp:101), so the multi-GPU layout is a contiguous split of the flat
 slice index with no collective on the data path.  NCCL is used only to
-gather per-rank results for verification.
+gather per-rank results for verification and to sum per-rank MRE partials.
 """
 from __future__ import annotations
 
@@ -46,3 +46,20 @@ def gather_slices(local, total: int, world: int, rank: int, group=None) -> List:
     bufs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(bufs, pad, group=group)
     return [bufs[r][: hi - lo] for r, (lo, hi) in enumerate(sizes)]
+
+
+def allreduce_error(acc, group=None):
+    """Sum every rank's ErrorAccum (num, den) into a whole-job accumulator
+    (f64 all-reduce): the normalized L1 error composes
+    exactly as eval.cpp:55-75 accumulates it across slices."""
+    import torch
+    import torch.distributed as dist
+    from .evaluation import ErrorAccum
+
+    t = torch.tensor([acc.num, acc.den], dtype=torch.float64)
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda()
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    out = ErrorAccum()
+    out.num, out.den = float(t[0]), float(t[1])
+    return out

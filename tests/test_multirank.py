@@ -70,6 +70,58 @@ def test_sharded_run_equals_single_process(tmp_path, oracle, total):
     assert np.array_equal(got.view(np.uint32), np.stack(want).view(np.uint32))
 
 
+def _mre_worker(rank, world, port, total, n, d, out_dir):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    import torch
+    import torch.distributed as dist
+    from oracle_bindings import Oracle
+    from paper_2409_16997_b200.evaluation import ErrorAccum
+    from paper_2409_16997_b200.sharding import allreduce_error, shard_range
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    o = Oracle()
+    lo, hi = shard_range(total, world, rank)
+    acc = ErrorAccum()
+    for s in range(lo, hi):
+        q, k, v = o.slice_inputs("normal", n, d, b=s // 4, h=s % 4)
+        qc, qs = o.quantize_per_row(q)
+        kc, ks = o.quantize_per_row(k)
+        vc, vs = o.quantize_per_tensor(v)
+        got = o.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, 64)
+        acc.add(torch.from_numpy(o.reference_attention(q, k, v)), torch.from_numpy(got))
+    tot = allreduce_error(acc)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "mre.npy"), np.array([tot.num, tot.den]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_mre_equals_single_process(tmp_path, oracle):
+    """Per-rank (num, den) partials summed across ranks give the single-process
+    MRE."""
+    import torch
+    import torch.multiprocessing as mp
+    from paper_2409_16997_b200.evaluation import ErrorAccum
+    n, d, world, total = 64, 16, 2, 5
+    mp.spawn(_mre_worker, args=(world, _free_port(), total, n, d, str(tmp_path)), nprocs=world,
+             join=True)
+    num, den = np.load(tmp_path / "mre.npy")
+    acc = ErrorAccum()
+    for s in range(total):
+        q, k, v = oracle.slice_inputs("normal", n, d, b=s // 4, h=s % 4)
+        qc, qs = oracle.quantize_per_row(q)
+        kc, ks = oracle.quantize_per_row(k)
+        vc, vs = oracle.quantize_per_tensor(v)
+        got = oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, 64)
+        acc.add(torch.from_numpy(oracle.reference_attention(q, k, v)), torch.from_numpy(got))
+    assert abs(num / den - acc.ratio()) <= 1e-12 * acc.ratio()
+
+
 @pytest.mark.gpu
 def test_bench_two_ranks_share_one_gpu(tmp_path):
     """bench.py's N>1 path (torchrun, per-rank shards, max-over-ranks timing,
