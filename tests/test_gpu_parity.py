@@ -315,7 +315,9 @@ def test_fast_mode_both_kernels_agree(ifa, oracle, n, d, causal, monkeypatch):
 @pytest.mark.parametrize("n,d,sqrt_d,causal", [(128, 128, False, False), (384, 128, True, False),
                                                (1024, 64, False, False), (2048, 128, False, False),
                                                (128, 64, False, True), (384, 128, False, True),
-                                               (1024, 128, True, True), (2048, 64, False, True)])
+                                               (1024, 128, True, True), (2048, 64, False, True),
+                                               (256, 100, False, False), (256, 48, True, True),
+                                               (512, 16, False, False)])
 def test_fast_mode_pp_kernel(ifa, oracle, dist, n, d, sqrt_d, causal, monkeypatch):
     """The two-Q-tile kernel (csrc/attn_pp.cu: fast, Bc = 128, n % 128 == 0;
     P.V as exact fp16 integers into an f32 TMEM accumulator) meets the
