@@ -1,6 +1,7 @@
 // attn_pp.cu -- tolerance-mode INT-FlashAttention forward with two Q tiles
-// per CTA in ping-pong (IFA_FLAG_FAST, non-causal, every KV block one
-// 128-key tile).  Same algorithm as attention.cpp:235-357 per block: exact
+// per CTA (IFA_FLAG_FAST, causal or not, every KV block one 128-key tile,
+// n % 128 == 0), also instantiated for the half-INT8 and FP8 variants (see
+// the MODE comment below).  Same algorithm as attention.cpp:235-357 per block: exact
 // int32 S = Q.K^T (tcgen05.mma kind::i8), dequantize, running row max,
 // requantize P to integer codes round(127 * exp(s - m)), O = O*alpha + P.V,
 // l = l*alpha + sum(codes), O * sV / l at the end.
@@ -184,15 +185,6 @@ __device__ __forceinline__ void mma_f16_ss(uint32_t d_tmem, uint64_t a_desc, uin
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
-                                           uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
 
