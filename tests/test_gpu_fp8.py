@@ -74,7 +74,8 @@ def _check(oracle, got, want, v):
 
 @pytest.mark.parametrize("dist", ["normal", "uniform"])
 @pytest.mark.parametrize("n,d,sqrt_d", [(128, 64, False), (200, 64, True), (1024, 64, False),
-                                        (96, 128, False), (333, 128, True), (1024, 128, False)])
+                                        (96, 128, False), (333, 128, True), (1024, 128, False),
+                                        (256, 128, True), (384, 64, True)])
 def test_fp8_attention_matches_oracle(ifa, oracle, dist, n, d, sqrt_d):
     q, k, v = oracle.slice_inputs(dist, n, d, seed=19)
     cfg = ifa.AttentionConfig(ifa.BlockSpec(64, 64), apply_sqrt_d_scaling=sqrt_d)

@@ -5,8 +5,9 @@ attention weights in f32; the sm_100a kernel feeds both to the tensor core
 as fp16 with f32 accumulation, so the output is checked within a tolerance:
 
 - MRE(GPU, oracle) <= 2e-3, and max|dO| <= 4e-3 * max|V| (fp16 weights and
-  V carry 2^-11 relative rounding each; both sides normalise by the same row
-  sum of fp16 weights);
+  V carry 2^-11 relative rounding each; the 16-warp kernel's row sum is the
+  tensor core's P.1 over the same fp16 weights, the two-Q-tile kernel
+  (n % 128 == 0) sums the f32 weights);
 - the GPU's error against the fp64 reference_attention is within 1% (+1e-5)
   of the reference algorithm's own error -- the fp16 steps must not change
   the accuracy the INT8 Q/K quantization sets.
@@ -58,10 +59,11 @@ def test_half_int8_matches_oracle(ifa, oracle, dist, n, d):
     _check(oracle, got.cpu().numpy(), want, v)
 
 
+@pytest.mark.parametrize("n", [300, 256])  # 256: the two-Q-tile pipeline
 @pytest.mark.parametrize("br,bc,sqrt_d", [(64, 64, True), (128, 128, False), (16, 48, True),
                                           (1, 1000, False)])
-def test_half_int8_blocks_and_scaling(ifa, oracle, br, bc, sqrt_d):
-    q, k, v = oracle.slice_inputs("normal", 300, 128, seed=5)
+def test_half_int8_blocks_and_scaling(ifa, oracle, br, bc, sqrt_d, n):
+    q, k, v = oracle.slice_inputs("normal", n, 128, seed=5)
     got, qq, kq = _run(ifa, q, k, v, br, bc, sqrt_d)
     want = _oracle(oracle, qq, kq, v, br, bc, sqrt_d)
     _check(oracle, got.cpu().numpy(), want, v)
