@@ -110,7 +110,8 @@ int ifa_int_flash_fwd(const int8_t* q, const float* sq, const int8_t* k, const f
  * ifa_int_flash_fwd_v16: ifa_int_flash_fwd with those fp16 codes supplied,
  *   so the two-Q-tile kernel (IFA_FLAG_FAST, Bc = 128, n % 128 == 0, d in
  *   {64, 128}; csrc/attn_pp.cu) skips its own conversion.  Any other case
- *   runs exactly ifa_int_flash_fwd on the int8 v (no audit). */
+ *   runs exactly ifa_int_flash_fwd on the int8 v (no audit), which for other
+ *   n converts V into a padded fp16 copy itself. */
 int ifa_quantize_per_tensor_v16(const float* x, int64_t slices, int64_t rows, int64_t cols,
                                 int8_t* codes, uint16_t* codes_f16, float* slice_scales,
                                 void* workspace, int64_t* nonfinite_index, void* stream);

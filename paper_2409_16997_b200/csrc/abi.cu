@@ -213,7 +213,7 @@ int ifa_int_flash_fwd_v16(const int8_t* q, const float* sq, const int8_t* k, con
     ifa_b200::AttnArgs a{q, sq, k, sk, v, sv, o, nullptr, slices, n, d, d, bc, flags};
     const bool aligned = ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) |
                            reinterpret_cast<uintptr_t>(v_f16)) % 16) == 0;
-    if ((d == 64 || d == 128) && aligned && ifa_b200::int_flash_pp_eligible(a)) {
+    if ((d == 64 || d == 128) && n % 128 == 0 && aligned && ifa_b200::int_flash_pp_eligible(a)) {
         const cudaError_t e =
             ifa_b200::launch_int_flash_pp(a, v_f16, static_cast<cudaStream_t>(stream));
         return e == cudaSuccess ? IFA_OK : cuda_fail(e, "int_flash_attention");

@@ -1,6 +1,6 @@
 // attn_pp.cu -- tolerance-mode INT-FlashAttention forward with two Q tiles
-// per CTA (IFA_FLAG_FAST, causal or not, every KV block one 128-key tile,
-// n % 128 == 0), also instantiated for the half-INT8 and FP8 variants (see
+// per CTA (IFA_FLAG_FAST, causal or not, every KV block one 128-key tile),
+// also instantiated for the half-INT8 and FP8 variants (see
 // the MODE comment below).  Same algorithm as attention.cpp:235-357 per block: exact
 // int32 S = Q.K^T (tcgen05.mma kind::i8), dequantize, running row max,
 // requantize P to integer codes round(127 * exp(s - m)), O = O*alpha + P.V,
@@ -28,7 +28,8 @@
 // 32-byte runs, MMA keys 64h + 16 t0 + 2k' + e for k = 8h + k' (a layout
 // without shared-memory bank conflicts); the fp16 V tile is loaded with its
 // rows permuted the same way (smem row 64h + 16t + 2k' + e <- key 64h + 8k' +
-// 2t + e) by a 5-D tensor map.  Needs n % 128 == 0.
+// 2t + e) by a 5-D tensor map over a V copy padded to a multiple of 128 rows
+// per slice; a ragged last tile masks its missing keys.
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -88,6 +89,7 @@ struct Params {
     const float* sv;
     float* o;
     int32_t n, d;
+    int32_t n_pad;  // rows per slice of the fp16 V buffer (n rounded up to 128)
     float sk_mul;  // log2(e) [* 1/sqrt(d)]: scores are kept in the log2 domain
     uint32_t flags;
     int32_t pairs, slices, items;
@@ -208,7 +210,9 @@ __device__ __forceinline__ void mma_f8_ss(uint32_t d_tmem, uint64_t a_desc, uint
         : "memory");
 }
 
-template <int D, bool CAUSAL, int MODE>
+// RAGGED: n is not a multiple of 128 (the last KV tile masks missing keys);
+// a template parameter so the common case carries no masking code.
+template <int D, bool CAUSAL, int MODE, bool RAGGED>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     int_flash_pp_kernel(const __grid_constant__ CUtensorMap tm_q,
                         const __grid_constant__ CUtensorMap tm_k,
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
     const int32_t n = p.n;
-    const int32_t J = n / BN;  // KV tiles of a slice (n % 128 == 0)
+    const int32_t J = (n + BN - 1) / BN;  // KV tiles of a slice
     // compile-time: the non-causal instantiation carries no masking or
     // per-group tile-count logic (it measured 20% slower with them at run time)
     constexpr bool causal = CAUSAL;
@@ -297,7 +301,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         const float c8 = __fdiv_rn(p.sk_mul, __fmul_rn(p.sq[slice], p.sk[slice]));
                         k4 = make_float4(c8, c8, c8, c8);
                     } else {
-                        k4 = __ldg(reinterpret_cast<const float4*>(sk_slice + key0) + lane);
+                        const int32_t key = key0 + 4 * lane;
+                        if (key + 3 < n) {
+                            k4 = __ldg(reinterpret_cast<const float4*>(sk_slice + key));
+                        } else {  // ragged tail (the keys are masked, but stay in bounds)
+                            k4.x = key + 0 < n ? sk_slice[key + 0] : 0.0f;
+                            k4.y = key + 1 < n ? sk_slice[key + 1] : 0.0f;
+                            k4.z = key + 2 < n ? sk_slice[key + 2] : 0.0f;
+                            k4.w = key + 3 < n ? sk_slice[key + 3] : 0.0f;
+                        }
                         k4.x *= p.sk_mul;
                         k4.y *= p.sk_mul;
                         k4.z *= p.sk_mul;
@@ -309,7 +321,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         tma_load_3d(sm.k[ks], &tm_k, &sm.k_full[ks], 0, key0, slice, pol_keep);
                         if (i >= VST) bar_wait(b_v_empty + 8 * vs, vr.phase ^ 1u);
                         mbar_arrive_expect_tx(&sm.v_full[vs], BN * D * 2);
-                        const int32_t tile = (slice * n + key0) / 64;  // 64-key halves
+                        const int32_t tile = (slice * p.n_pad + key0) / 64;  // 64-key halves
 #pragma unroll
                         for (int h = 0; h < D / 64; ++h)
                             tma_load_5d(sm.v[vs] + h * BN * 128, &tm_v, &sm.v_full[vs], 64 * h,
@@ -504,8 +516,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 // rest of the tile, instantiated twice so the diagonal masking of
                 // the causal kernel never becomes per-element predicated code on the
                 // other tiles
-                auto rest = [&](auto diag_tag) {
-                    constexpr bool dmask = decltype(diag_tag)::value;  // keys > row masked
+                auto rest = [&](auto mask_tag) {
+                    constexpr bool dmask = decltype(mask_tag)::value;  // keys > kmax masked
+                    // last visible key of each row in this tile (masked tiles only):
+                    // the causal diagonal and / or the ragged end of the sequence
+                    int32_t kmax[2] = {BN - 1, BN - 1};
+                    if (dmask) {
+#pragma unroll
+                        for (int r = 0; r < 2; ++r) {
+                            if (RAGGED && n - j * BN - 1 < kmax[r]) kmax[r] = n - j * BN - 1;
+                            if (causal && j == diag && row0 + 8 * r < kmax[r]) kmax[r] = row0 + 8 * r;
+                        }
+                    }
                     if (dmask) {
     #pragma unroll
                         for (int k = 0; k < 16; ++k)
@@ -513,7 +535,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             for (int r = 0; r < 2; ++r)
     #pragma unroll
                                 for (int e = 0; e < 2; ++e)
-                                    if (8 * k + 2 * static_cast<int32_t>(t0) + e > row0 + 8 * r)
+                                    if (8 * k + 2 * static_cast<int32_t>(t0) + e > kmax[r])
                                         u[4 * k + 2 * r + e] = -__int_as_float(0x7f800000);
                     }
                     float cr[2], alpha[2];
@@ -554,8 +576,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             float2 c = MODE == kModeCodes ? fsub2(fadd2(y, f2(kMagic)), f2(kMagic)) : y;
                             if (dmask) {  // masked keys weigh 0 (also when sQ == 0)
                                 const int32_t key = 8 * k + 2 * static_cast<int32_t>(t0);
-                                if (key > row0 + 8 * r) c.x = 0.0f;
-                                if (key + 1 > row0 + 8 * r) c.y = 0.0f;
+                                if (key > kmax[r]) c.x = 0.0f;
+                                if (key + 1 > kmax[r]) c.y = 0.0f;
                             }
                             ls[r] = fadd2(ls[r], c);
                             const __half2 h = __floats2half2_rn(c.x, c.y);
@@ -606,10 +628,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                     for (int r = 0; r < 2; ++r) l[r] = __fmaf_rn(l[r], alpha[r], ls[r].x + ls[r].y);
                 };
-                if (causal && j == diag)
-                    rest(std::true_type{});
-                else
+                if constexpr (causal || RAGGED) {
+                    if ((causal && j == diag) || (RAGGED && (j + 1) * BN > n))
+                        rest(std::true_type{});
+                    else
+                        rest(std::false_type{});
+                } else {
                     rest(std::false_type{});
+                }
                 kv.advance();
                 ++tc;
             }
@@ -666,16 +692,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
 }
 
-// int8 codes [rows][pitch] -> fp16 [rows][D] (columns >= pitch are zero).
-__global__ void codes_to_f16_kernel(const int8_t* __restrict__ src, int64_t rows, int64_t pitch,
-                                    int dcols, __half* __restrict__ dst) {
-    const int64_t total = rows * dcols;
+// int8 codes [slices][n][pitch] -> fp16 [slices][n_pad][D] (columns >= pitch
+// and rows >= n are zero).
+__global__ void codes_to_f16_kernel(const int8_t* __restrict__ src, int64_t slices, int64_t n,
+                                    int64_t n_pad, int64_t pitch, int dcols,
+                                    __half* __restrict__ dst) {
+    const int64_t total = slices * n_pad * dcols;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total / 8;
          i += stride) {
-        const int64_t e = 8 * i, r = e / dcols, c = e - r * dcols;
+        const int64_t e = 8 * i, rp = e / dcols, c = e - rp * dcols;
+        const int64_t sl = rp / n_pad, rr = rp - sl * n_pad, r = sl * n + rr;
         __align__(16) __half h[8];
-        if (c + 8 <= pitch && (pitch % 8) == 0) {
+        if (rr >= n) {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) h[t] = __float2half_rn(0.0f);
+        } else if (c + 8 <= pitch && (pitch % 8) == 0) {
             const uint2 w = *reinterpret_cast<const uint2*>(src + r * pitch + c);
             const int8_t* b = reinterpret_cast<const int8_t*>(&w);
 #pragma unroll
@@ -751,18 +783,27 @@ static cudaError_t run(const void* q, const void* k, const __half* v16, const Pa
     CUtensorMap tq, tk, tv;
     if (!make_map_codes(&tq, static_cast<const int8_t*>(q), p.slices, p.n, pitch, D) ||
         !make_map_codes(&tk, static_cast<const int8_t*>(k), p.slices, p.n, pitch, D) ||
-        !make_map_v16(&tv, v16, p.slices, p.n, D))
+        !make_map_v16(&tv, v16, p.slices, p.n_pad, D))
         return cudaErrorInvalidValue;
     const size_t smem = sizeof(Smem<D>) + 1024;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(int_flash_pp_kernel<D, false, MODE>,
+        cudaError_t e = cudaFuncSetAttribute(int_flash_pp_kernel<D, false, MODE, false>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
-        if (e == cudaSuccess && MODE == kModeCodes)
-            e = cudaFuncSetAttribute(int_flash_pp_kernel<D, true, MODE>,
+        if (e == cudaSuccess && MODE == kModeCodes) {
+            e = cudaFuncSetAttribute(int_flash_pp_kernel<D, true, MODE, false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem));
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(int_flash_pp_kernel<D, false, MODE, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(int_flash_pp_kernel<D, true, MODE, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+        }
         if (e != cudaSuccess) return e;
         configured = true;
     }
@@ -774,10 +815,19 @@ static cudaError_t run(const void* q, const void* k, const __half* v16, const Pa
         if (sms <= 0) sms = 148;
     }
     const int grid = p.items < sms ? p.items : sms;
-    if (MODE == kModeCodes && causal)
-        int_flash_pp_kernel<D, true, MODE><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
-    else
-        int_flash_pp_kernel<D, false, MODE><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+    const bool ragged = p.n % BN != 0;
+    if constexpr (MODE == kModeCodes) {
+        if (causal && ragged)
+            int_flash_pp_kernel<D, true, MODE, true><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+        else if (causal)
+            int_flash_pp_kernel<D, true, MODE, false><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+        else if (ragged)
+            int_flash_pp_kernel<D, false, MODE, true><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+        else
+            int_flash_pp_kernel<D, false, MODE, false><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+    } else {  // half-INT8 / FP8: non-causal, n % 128 == 0 (float_weights_pp_eligible)
+        int_flash_pp_kernel<D, false, MODE, false><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+    }
     return cudaGetLastError();
 }
 
@@ -790,6 +840,7 @@ static Params make_params(const float* sq, const float* sk, const float* sv, flo
     p.o = o;
     p.n = static_cast<int32_t>(n);
     p.d = static_cast<int32_t>(d);
+    p.n_pad = static_cast<int32_t>((n + BN - 1) / BN * BN);
     p.flags = flags;
     p.sk_mul = kLog2e * ((flags & IFA_FLAG_SQRT_D) ? 1.0f / sqrtf(static_cast<float>(d)) : 1.0f);
     const int32_t q_tiles = static_cast<int32_t>((n + BM - 1) / BM);
@@ -813,16 +864,18 @@ static cudaError_t launch(const AttnArgs& a, const uint16_t* v16_given, cudaStre
     }
     __half* v16 = const_cast<__half*>(reinterpret_cast<const __half*>(v16_given));
     __half* owned = nullptr;
-    const int64_t rows = a.slices * a.n;
+    const int64_t n_pad = (a.n + BN - 1) / BN * BN;
+    const int64_t rows = a.slices * n_pad;
     cudaError_t e = cudaSuccess;
+    if (v16 && n_pad != a.n) return cudaErrorInvalidValue;  // a given copy is unpadded
     if (!v16) {  // fp16 copy of the V codes (the caller may pass one: ifa_int_flash_fwd_v16)
         e = cudaMallocAsync(reinterpret_cast<void**>(&owned), rows * D * 2, stream);
         if (e != cudaSuccess) return e;
         v16 = owned;
         int64_t blocks = (rows * D / 8 + 255) / 256;
         if (blocks > 148 * 16) blocks = 148 * 16;
-        codes_to_f16_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(a.v, rows, a.pitch,
-                                                                                D, v16);
+        codes_to_f16_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+            a.v, a.slices, a.n, n_pad, a.pitch, D, v16);
     }
     const Params p = make_params(a.sq, a.sk, a.sv, a.o, a.slices, a.n, a.d, a.flags);
     e = run<D, kModeCodes>(a.q, a.k, v16, p, a.pitch, (a.flags & IFA_FLAG_CAUSAL) != 0, stream);
@@ -838,7 +891,7 @@ bool int_flash_pp_eligible(const AttnArgs& a) {
     const int64_t bc = a.bc < a.n ? a.bc : a.n;
     const bool tiles_are_blocks = bc == pp::BN || (bc == a.n && a.n <= pp::BN);
     return (a.flags & IFA_FLAG_FAST) &&
-           a.audit == nullptr && tiles_are_blocks && a.n % 128 == 0 && a.d <= 128;
+           a.audit == nullptr && tiles_are_blocks && a.d <= 128;
 }
 
 cudaError_t launch_int_flash_pp(const AttnArgs& a, const uint16_t* v16, cudaStream_t stream) {

@@ -50,7 +50,7 @@ class AttentionPlan:
         self.bad = torch.full((1,), _INT64_MAX, dtype=torch.int64, device=dev)
         # fp16 V codes for the two-Q-tile kernel, written by the V quantizer
         self.v16 = torch.empty(shape, dtype=torch.float16, device=dev) \
-            if self.uses_pp_kernel() and d in (64, 128) else None
+            if self.uses_pp_kernel() and d in (64, 128) and n % 128 == 0 else None
         self.graph: Optional[torch.cuda.CUDAGraph] = None
         self._graph_io = None
 
@@ -102,12 +102,11 @@ class AttentionPlan:
 
     def uses_pp_kernel(self) -> bool:
         """True when ifa_int_flash_fwd takes the two-Q-tile tolerance kernel
-        (csrc/attn_pp.cu: fast mode, Bc = 128, n % 128 == 0),
+        (csrc/attn_pp.cu: fast mode, Bc = 128),
         which first converts the V codes to fp16 (one extra launch)."""
         bc = min(self.bc, self.n)
         blocks = bc == 128 or (bc == self.n and self.n <= 128)
-        return bool(self.flags & _lib.FLAG_FAST) and \
-            blocks and self.n % 128 == 0 and self.d <= 128 and \
+        return bool(self.flags & _lib.FLAG_FAST) and blocks and self.d <= 128 and \
             os.environ.get("IFA_B200_NO_PP", "") != "1"
 
     def launches_per_step(self) -> int:
