@@ -265,8 +265,9 @@ def _fast_close(got, want, vc, vs):
 @pytest.mark.parametrize("dist", ["normal", "uniform"])
 @pytest.mark.parametrize("causal", [False, True])
 def test_fast_mode_within_tolerance(ifa, oracle, n, d, dist, causal):
-    """n % 128 == 0 runs the two-Q-tile kernel (attn_pp.cu), other n % 32 == 0
-    shapes the quad-layout kernel (8 math warps), the rest the 16-warp one."""
+    """Bc = 128 runs the two-Q-tile kernel (attn_pp.cu) for every n, ragged n
+    through its padded-V / masked-tail instantiation; the one-tile kernels are
+    covered with IFA_B200_NO_PP=1 below."""
     _, (qc, qs, kc, ks, vc, vs) = _quantized_case(oracle, dist, n, d, seed=n + d)
     want = oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, 128,
                                       flags=2 if causal else 0)
