@@ -264,10 +264,13 @@ def _fast_close(got, want, vc, vs):
                                  (300, 100), (1000, 128), (1024, 64), (4096, 128)])
 @pytest.mark.parametrize("dist", ["normal", "uniform"])
 @pytest.mark.parametrize("causal", [False, True])
-def test_fast_mode_within_tolerance(ifa, oracle, n, d, dist, causal):
+@pytest.mark.parametrize("pp", [True, False])
+def test_fast_mode_within_tolerance(ifa, oracle, n, d, dist, causal, pp, monkeypatch):
     """Bc = 128 runs the two-Q-tile kernel (attn_pp.cu) for every n, ragged n
-    through its padded-V / masked-tail instantiation; the one-tile kernels are
-    covered with IFA_B200_NO_PP=1 below."""
+    through its padded-V / masked-tail instantiation; with IFA_B200_NO_PP=1 the
+    one-tile kernels (quad layout for n % 32 == 0, else 16 warps) run instead."""
+    if not pp:
+        monkeypatch.setenv("IFA_B200_NO_PP", "1")
     _, (qc, qs, kc, ks, vc, vs) = _quantized_case(oracle, dist, n, d, seed=n + d)
     want = oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, 128,
                                       flags=2 if causal else 0)
