@@ -648,10 +648,12 @@ __device__ __forceinline__ void softmax_quad(Smem<D>& sm, const Params& p, uint3
                 const int col = 8 * k + 2 * static_cast<int>(t0);
                 if (col < p.d) {
                     const float2 o = make_float2(acc[r][2 * k] * f, acc[r][2 * k + 1] * f);
-                    if (col + 1 < p.d)
+                    if (col + 1 < p.d && (p.d & 1) == 0) {  // 8-byte aligned pair
                         __stcs(reinterpret_cast<float2*>(orow + col), o);
-                    else
+                    } else {
                         orow[col] = o.x;
+                        if (col + 1 < p.d) orow[col + 1] = o.y;
+                    }
                 }
             }
         }

@@ -302,7 +302,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         k4 = make_float4(c8, c8, c8, c8);
                     } else {
                         const int32_t key = key0 + 4 * lane;
-                        if (key + 3 < n) {
+                        if (key + 3 < n &&
+                            (reinterpret_cast<uintptr_t>(sk_slice + key) & 15) == 0) {
                             k4 = __ldg(reinterpret_cast<const float4*>(sk_slice + key));
                         } else {  // ragged tail (the keys are masked, but stay in bounds)
                             k4.x = key + 0 < n ? sk_slice[key + 0] : 0.0f;
@@ -674,10 +675,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         const int col = 32 * c + 8 * k + 2 * static_cast<int>(t0);
                         const float2 v = make_float2(__uint_as_float(o[4 * k + 2 * r]) * f[r],
                                                      __uint_as_float(o[4 * k + 2 * r + 1]) * f[r]);
-                        if (col + 1 < p.d)
+                        if (col + 1 < p.d && (p.d & 1) == 0) {  // 8-byte aligned pair
                             __stcs(reinterpret_cast<float2*>(orow + col), v);
-                        else if (col < p.d)
+                        } else if (col < p.d) {
                             orow[col] = v.x;
+                            if (col + 1 < p.d) orow[col + 1] = v.y;
+                        }
                     }
                 }
             }
