@@ -57,3 +57,48 @@ def test_random_shapes_against_oracle(ifa, oracle, seed):
         else:
             assert np.array_equal(got[s].view(np.uint32), want.view(np.uint32)), \
                 (seed, n, d, bc, causal, sqrt_d)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_random_quantizer_shapes_bitwise(ifa, oracle, seed):
+    rng = np.random.default_rng(1000 + seed)
+    slices = int(rng.integers(1, 4))
+    rows = int(rng.choice([1, 3, 17, 64, 129, 500]))
+    cols = int(rng.choice([1, 2, 5, 16, 33, 64, 100, 128, 256]))
+    scale = float(rng.choice([1e-30, 1e-3, 1.0, 1e4]))
+    x = (rng.standard_normal((slices, rows, cols)) * scale).astype(np.float32)
+    if rng.integers(0, 4) == 0:
+        x[0] = 0.0  # an all-zero slice: scale 0, codes 0
+    xt = torch.from_numpy(x).cuda()
+    r = ifa.quantize_per_row(xt)
+    t = ifa.quantize_per_tensor(xt)
+    for s in range(slices):
+        qc, qs = oracle.quantize_per_row(x[s])
+        assert np.array_equal(r.values[s].cpu().numpy(), qc)
+        assert np.array_equal(r.scales[s].cpu().numpy().view(np.uint32), qs.view(np.uint32))
+        vc, vs = oracle.quantize_per_tensor(x[s])
+        assert np.array_equal(t.values[s].cpu().numpy(), vc)
+        assert np.float32(t.scale[s].item()) == np.float32(vs)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_float_weight_variants(ifa, oracle, seed):
+    """half-INT8 and FP8 (both kernels: n % 128 == 0 runs the two-Q-tile
+    pipeline) against their oracle restatements."""
+    rng = np.random.default_rng(2000 + seed)
+    n = int(rng.choice([1, 50, 128, 200, 256, 384]))
+    d = int(rng.choice([64, 128]))
+    sqrt_d = bool(rng.integers(0, 2))
+    bc = int(rng.choice([16, 64, 128, 1000]))
+    q, k, v = oracle.slice_inputs("normal" if seed % 2 else "uniform", n, d, seed=seed)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    cfg = ifa.AttentionConfig(ifa.BlockSpec(64, bc), apply_sqrt_d_scaling=sqrt_d)
+    qq, kq = ifa.quantize_per_row(dev(q)), ifa.quantize_per_row(dev(k))
+    got = ifa.half_int8_attention(qq, kq, dev(v), cfg).cpu().numpy()
+    want = oracle.half_int8_attention(qq.values.cpu().numpy(), qq.scales.cpu().numpy(),
+                                      kq.values.cpu().numpy(), kq.scales.cpu().numpy(), v,
+                                      64, bc, 1 if sqrt_d else 0)
+    assert oracle.mre(want, got) <= 2e-3
+    got8 = ifa.fp8_emulated_attention(dev(q), dev(k), dev(v), cfg).cpu().numpy()
+    want8 = oracle.fp8_attention(q, k, v, 64, bc, flags=1 if sqrt_d else 0)
+    assert oracle.mre(want8, got8) <= 2e-3
