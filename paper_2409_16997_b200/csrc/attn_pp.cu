@@ -89,7 +89,8 @@ struct Params {
     const float* sv;
     float* o;
     int32_t n, d;
-    int32_t n_pad;  // rows per slice of the fp16 V buffer (n rounded up to 128)
+    int32_t n_pad;    // rows per slice of the fp16 V buffer (n rounded up to 128)
+    int32_t o_pitch;  // floats per O row (even: the epilogue stores 8-byte pairs)
     float sk_mul;  // log2(e) [* 1/sqrt(d)]: scores are kept in the log2 domain
     uint32_t flags;
     int32_t pairs, slices, items;
@@ -669,18 +670,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
                     if (grow[r] >= n) continue;
-                    float* orow = p.o + (static_cast<int64_t>(slice) * n + grow[r]) * p.d;
+                    float* orow = p.o + (static_cast<int64_t>(slice) * n + grow[r]) * p.o_pitch;
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         const int col = 32 * c + 8 * k + 2 * static_cast<int>(t0);
                         const float2 v = make_float2(__uint_as_float(o[4 * k + 2 * r]) * f[r],
                                                      __uint_as_float(o[4 * k + 2 * r + 1]) * f[r]);
-                        if (col + 1 < p.d && (p.d & 1) == 0) {  // 8-byte aligned pair
+                        if (col + 1 < p.d)
                             __stcs(reinterpret_cast<float2*>(orow + col), v);
-                        } else if (col < p.d) {
+                        else if (col < p.d)
                             orow[col] = v.x;
-                            if (col + 1 < p.d) orow[col + 1] = v.y;
-                        }
                     }
                 }
             }
@@ -843,6 +842,7 @@ static Params make_params(const float* sq, const float* sk, const float* sv, flo
     p.o = o;
     p.n = static_cast<int32_t>(n);
     p.d = static_cast<int32_t>(d);
+    p.o_pitch = static_cast<int32_t>(d);
     p.n_pad = static_cast<int32_t>((n + BN - 1) / BN * BN);
     p.flags = flags;
     p.sk_mul = kLog2e * ((flags & IFA_FLAG_SQRT_D) ? 1.0f / sqrtf(static_cast<float>(d)) : 1.0f);
@@ -880,8 +880,26 @@ static cudaError_t launch(const AttnArgs& a, const uint16_t* v16_given, cudaStre
         codes_to_f16_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
             a.v, a.slices, a.n, n_pad, a.pitch, D, v16);
     }
-    const Params p = make_params(a.sq, a.sk, a.sv, a.o, a.slices, a.n, a.d, a.flags);
+    Params p = make_params(a.sq, a.sk, a.sv, a.o, a.slices, a.n, a.d, a.flags);
+    float* o_even = nullptr;  // odd d: rows of d + 1 floats, then compacted into a.o
+    if (a.d & 1) {
+        e = cudaMallocAsync(reinterpret_cast<void**>(&o_even),
+                            sizeof(float) * a.slices * a.n * (a.d + 1), stream);
+        if (e != cudaSuccess) {
+            if (owned) cudaFreeAsync(owned, stream);
+            return e;
+        }
+        p.o = o_even;
+        p.o_pitch = static_cast<int32_t>(a.d + 1);
+    }
     e = run<D, kModeCodes>(a.q, a.k, v16, p, a.pitch, (a.flags & IFA_FLAG_CAUSAL) != 0, stream);
+    if (o_even) {
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(a.o, sizeof(float) * a.d, o_even, sizeof(float) * (a.d + 1),
+                                  sizeof(float) * a.d, a.slices * a.n, cudaMemcpyDeviceToDevice,
+                                  stream);
+        cudaFreeAsync(o_even, stream);
+    }
     const cudaError_t e2 = owned ? cudaFreeAsync(owned, stream) : cudaSuccess;
     return e != cudaSuccess ? e : e2;
 }
