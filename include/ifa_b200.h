@@ -177,6 +177,20 @@ int ifa_int_flash_fwd_host(const int8_t* q, const float* sq, const int8_t* k, co
                            int64_t n, int64_t d, int64_t br, int64_t bc, uint32_t flags,
                            ifa_pcode_audit* audit, void* stream);
 
+/* Host-buffer forms of the §8(f) variants (what include/ifa_b200.hpp's
+ * ifa_gpu::half_int8_attention / fp8_emulated_attention call):
+ *   ifa_half_int8_fwd_host: int8 Q/K codes + per-row scales and f32 V (host)
+ *     -> f32 O (host); V is converted to fp16 on the device.
+ *   ifa_fp8_emulated_attention_host: f32 Q, K, V (host) -> f32 O (host): the
+ *     three e4m3 roundtrips and the FP8 forward; non-finite input returns
+ *     IFA_EINVAL "fp8_e4m3_roundtrip: non-finite input" (fp8.cpp:82-84). */
+int ifa_half_int8_fwd_host(const int8_t* q, const float* sq, const int8_t* k, const float* sk,
+                           const float* v, float* o, int64_t slices, int64_t n, int64_t d,
+                           int64_t br, int64_t bc, uint32_t flags, void* stream);
+int ifa_fp8_emulated_attention_host(const float* q, const float* k, const float* v, float* o,
+                                    int64_t slices, int64_t n, int64_t d, int64_t br,
+                                    int64_t bc, uint32_t flags, void* stream);
+
 /* Writes {127, 0, 1, 0, 0} into a device ifa_pcode_audit (async on stream). */
 int ifa_audit_init(ifa_pcode_audit* audit, void* stream);
 

@@ -82,4 +82,47 @@ inline ifa::FloatMatrix int_flash_attention(const ifa::QuantizedAttentionInputs&
     return out;
 }
 
+/// Drop-in for ifa::half_int8_attention (attention.hpp:93-96,
+/// attention.cpp:359-399): same signature and exceptions; O within the
+/// tolerance include/ifa_b200.h states (fp16 weights on the tensor core).
+inline ifa::FloatMatrix half_int8_attention(const ifa::QuantizedRows& q,
+                                            const ifa::QuantizedRows& k,
+                                            const ifa::FloatMatrix& v,
+                                            const ifa::AttentionConfig& cfg) {
+    const int64_t n = q.values.rows(), d = q.values.cols();
+    if (k.values.cols() != d) throw std::invalid_argument("half_int8_attention: q/k head dims differ");
+    if (k.values.rows() != v.rows())
+        throw std::invalid_argument("half_int8_attention: k/v row counts differ");
+    if (q.scales.len() != n || k.scales.len() != k.values.rows())
+        throw std::invalid_argument("half_int8_attention: scale length mismatch");
+    if (n < 1 || d < 1 || v.cols() < 1) throw std::invalid_argument("half_int8_attention: empty input");
+    if (k.values.rows() != n || v.cols() != d)
+        throw std::runtime_error("half_int8_attention: the sm_100a kernel takes q, k, v of one shape");
+    cfg.validate();
+    ifa::FloatMatrix out(n, d);
+    check(ifa_half_int8_fwd_host(q.values.data(), q.scales.data(), k.values.data(), k.scales.data(),
+                                 v.data(), out.data(), 1, n, d, cfg.blocks.Br, cfg.blocks.Bc,
+                                 cfg.apply_sqrt_d_scaling ? IFA_FLAG_SQRT_D : 0u, nullptr));
+    return out;
+}
+
+/// Drop-in for ifa::fp8_emulated_attention (attention.hpp:98-101,
+/// attention.cpp:401-407), run natively in FP8 (tcgen05 kind::f8f6f4).
+inline ifa::FloatMatrix fp8_emulated_attention(const ifa::FloatMatrix& q,
+                                               const ifa::FloatMatrix& k,
+                                               const ifa::FloatMatrix& v,
+                                               const ifa::AttentionConfig& cfg) {
+    const int64_t n = q.rows(), d = q.cols();
+    if (n < 1 || d < 1 || v.cols() < 1) throw std::invalid_argument("fp8_emulated_attention: empty input");
+    if (k.rows() != n || k.cols() != d || v.rows() != n || v.cols() != d)
+        throw std::runtime_error("fp8_emulated_attention: the sm_100a kernel takes q, k, v of one shape");
+    cfg.validate();
+    ifa::FloatMatrix out(n, d);
+    check(ifa_fp8_emulated_attention_host(q.data(), k.data(), v.data(), out.data(), 1, n, d,
+                                          cfg.blocks.Br, cfg.blocks.Bc,
+                                          cfg.apply_sqrt_d_scaling ? IFA_FLAG_SQRT_D : 0u,
+                                          nullptr));
+    return out;
+}
+
 }  // namespace ifa_gpu

@@ -37,6 +37,8 @@ EXPORTED_SYMBOLS = (
     "ifa_quantize_per_row_host",
     "ifa_quantize_per_tensor_host",
     "ifa_int_flash_fwd_host",
+    "ifa_half_int8_fwd_host",
+    "ifa_fp8_emulated_attention_host",
     "ifa_tensor_save",
     "ifa_tensor_info",
     "ifa_tensor_load",
@@ -108,6 +110,12 @@ def load() -> C.CDLL:
     lib.ifa_int_flash_fwd_host.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64,
                                            u32, vp, vp]
     lib.ifa_int_flash_fwd_host.restype = C.c_int
+    lib.ifa_half_int8_fwd_host.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, u32,
+                                           vp]
+    lib.ifa_half_int8_fwd_host.restype = C.c_int
+    lib.ifa_fp8_emulated_attention_host.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64, i64,
+                                                    u32, vp]
+    lib.ifa_fp8_emulated_attention_host.restype = C.c_int
     i32 = C.c_int32
     lib.ifa_tensor_save.argtypes = [C.c_char_p, i32, vp, i64, i64]
     lib.ifa_tensor_save.restype = C.c_int

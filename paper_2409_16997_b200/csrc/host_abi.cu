@@ -219,4 +219,97 @@ int ifa_int_flash_fwd_host(const int8_t* q, const float* sq, const int8_t* k, co
     return IFA_OK;
 }
 
+int ifa_half_int8_fwd_host(const int8_t* q, const float* sq, const int8_t* k, const float* sk,
+                           const float* v, float* o, int64_t slices, int64_t n, int64_t d,
+                           int64_t br, int64_t bc, uint32_t flags, void* stream) {
+    ifa_b200::set_error(IFA_OK, "");
+    if (slices < 0 || n < 1 || d < 1)
+        return ifa_b200::set_error(IFA_EINVAL, "half_int8_attention: empty input");
+    if (slices == 0) return IFA_OK;
+    if (!q || !sq || !k || !sk || !v || !o)
+        return ifa_b200::set_error(IFA_EINVAL, "half_int8_attention: null pointer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t elems = static_cast<size_t>(slices) * n * d;
+    const size_t rows = static_cast<size_t>(slices) * n;
+    cudaError_t e = g_ws.reserve(2 * align256(elems) + 2 * align256(rows * 4) +
+                                 2 * align256(elems * 4) + align256(elems * 2) + 256);
+    if (e != cudaSuccess) return cuda_status(e, "half_int8_attention: workspace");
+    Carver c{static_cast<char*>(g_ws.ptr)};
+    int8_t* dq = c.take<int8_t>(elems);
+    int8_t* dk = c.take<int8_t>(elems);
+    float* dsq = c.take<float>(rows);
+    float* dsk = c.take<float>(rows);
+    float* dv = c.take<float>(elems);
+    uint16_t* dv16 = c.take<uint16_t>(elems);
+    float* dout = c.take<float>(elems);
+    if ((e = cudaMemcpyAsync(dq, q, elems, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dk, k, elems, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dsq, sq, rows * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dsk, sk, rows * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dv, v, elems * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+        return cuda_status(e, "half_int8_attention: copy in");
+    int rc = ifa_convert_f16(dv, static_cast<int64_t>(elems), dv16, stream);
+    if (rc != IFA_OK) return rc;
+    rc = ifa_half_int8_fwd(dq, dsq, dk, dsk, dv16, dout, slices, n, d, br, bc, flags, stream);
+    if (rc != IFA_OK) return rc;
+    if ((e = cudaMemcpyAsync(o, dout, elems * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(st)) != cudaSuccess)
+        return cuda_status(e, "half_int8_attention: copy out");
+    return IFA_OK;
+}
+
+int ifa_fp8_emulated_attention_host(const float* q, const float* k, const float* v, float* o,
+                                    int64_t slices, int64_t n, int64_t d, int64_t br,
+                                    int64_t bc, uint32_t flags, void* stream) {
+    ifa_b200::set_error(IFA_OK, "");
+    if (slices < 0 || n < 1 || d < 1)
+        return ifa_b200::set_error(IFA_EINVAL, "fp8_emulated_attention: empty input");
+    if (slices == 0) return IFA_OK;
+    if (!q || !k || !v || !o)
+        return ifa_b200::set_error(IFA_EINVAL, "fp8_emulated_attention: null pointer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t elems = static_cast<size_t>(slices) * n * d;
+    cudaError_t e = g_ws.reserve(3 * align256(elems * 4) + 3 * align256(elems) +
+                                 align256(elems * 2) + 3 * align256(slices * 4) +
+                                 align256(slices * 4) + align256(8) + align256(elems * 4) + 256);
+    if (e != cudaSuccess) return cuda_status(e, "fp8_emulated_attention: workspace");
+    Carver c{static_cast<char*>(g_ws.ptr)};
+    const float* hx[3] = {q, k, v};
+    float* dx[3];
+    uint8_t* codes[3];
+    float* scales[3];
+    for (int i = 0; i < 3; ++i) dx[i] = c.take<float>(elems);
+    for (int i = 0; i < 3; ++i) codes[i] = c.take<uint8_t>(elems);
+    uint16_t* dv16 = c.take<uint16_t>(elems);
+    for (int i = 0; i < 3; ++i) scales[i] = c.take<float>(slices);
+    uint32_t* ws = c.take<uint32_t>(slices);
+    int64_t* bad = c.take<int64_t>(1);
+    float* dout = c.take<float>(elems);
+    const int64_t none = kNoIndex;
+    if ((e = cudaMemcpyAsync(bad, &none, 8, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+        return cuda_status(e, "fp8_emulated_attention: copy in");
+    for (int i = 0; i < 3; ++i) {
+        if ((e = cudaMemcpyAsync(dx[i], hx[i], elems * 4, cudaMemcpyHostToDevice, st)) !=
+            cudaSuccess)
+            return cuda_status(e, "fp8_emulated_attention: copy in");
+        const int rc = ifa_fp8_quantize_per_tensor(dx[i], slices, n, d, codes[i],
+                                                   i == 2 ? dv16 : nullptr, scales[i], ws, bad,
+                                                   stream);
+        if (rc != IFA_OK) return rc;
+    }
+    int64_t hbad = kNoIndex;
+    if ((e = cudaMemcpyAsync(&hbad, bad, 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(st)) != cudaSuccess)
+        return cuda_status(e, "fp8_emulated_attention");
+    if (hbad != kNoIndex)  // fp8.cpp:82-84
+        return ifa_b200::set_error(IFA_EINVAL, "fp8_e4m3_roundtrip: non-finite input");
+    const int rc = ifa_fp8_attention_fwd(codes[0], scales[0], codes[1], scales[1], dv16,
+                                         scales[2], dout, slices, n, d, br, bc, flags, stream);
+    if (rc != IFA_OK) return rc;
+    if ((e = cudaMemcpyAsync(o, dout, elems * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(st)) != cudaSuccess)
+        return cuda_status(e, "fp8_emulated_attention: copy out");
+    return IFA_OK;
+}
+
 }  // extern "C"

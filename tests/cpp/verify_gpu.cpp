@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include "ifa/attention.hpp"
+#include "ifa/eval.hpp"
 #include "ifa/generate.hpp"
 #include "ifa/quant.hpp"
 #include "ifa/verify.hpp"
@@ -94,6 +96,37 @@ int main() {
                 ++bad;
         }
         std::printf("%s quantize_per_row / quantize_per_tensor drop-ins bitwise (24 cases)\n",
+                    bad ? "FAIL" : "ok  ");
+        failures += bad;
+    }
+    // §8(f) drop-ins: half_int8_attention and fp8_emulated_attention against the
+    // reference library on the same inputs (tolerance: MRE <= 2e-3).
+    {
+        int bad = 0;
+        for (int t = 0; t < 6; ++t) {
+            const int64_t n = (t % 2) ? 256 : 200, d = (t % 3 == 0) ? 64 : 128;
+            auto gen = [&](int role) {
+                return ifa::generate(t % 2 ? ifa::ActivationSpec::uniform(-0.5, 0.5, 77 + 3 * t + role)
+                                           : ifa::ActivationSpec::normal(0.0, 1.0, 77 + 3 * t + role),
+                                     n, d);
+            };
+            const ifa::FloatMatrix q = gen(0), k = gen(1), v = gen(2);
+            ifa::AttentionConfig cfg;
+            cfg.blocks = ifa::BlockSpec{64, t < 3 ? 64 : 128};
+            cfg.apply_sqrt_d_scaling = t % 2 == 0;
+            const ifa::QuantizedRows qr = ifa::quantize_per_row(q), kr = ifa::quantize_per_row(k);
+            const ifa::FloatMatrix h_want = ifa::half_int8_attention(qr, kr, v, cfg);
+            const ifa::FloatMatrix h_got = ifa_gpu::half_int8_attention(qr, kr, v, cfg);
+            const ifa::FloatMatrix f_want = ifa::fp8_emulated_attention(q, k, v, cfg);
+            const ifa::FloatMatrix f_got = ifa_gpu::fp8_emulated_attention(q, k, v, cfg);
+            const double e_h = ifa::mre(h_want, h_got), e_f = ifa::mre(f_want, f_got);
+            if (!(e_h <= 2e-3) || !(e_f <= 2e-3)) {
+                std::printf("FAIL  n=%lld d=%lld half MRE %.3g fp8 MRE %.3g\n",
+                            static_cast<long long>(n), static_cast<long long>(d), e_h, e_f);
+                ++bad;
+            }
+        }
+        std::printf("%s half_int8_attention / fp8_emulated_attention drop-ins within tolerance\n",
                     bad ? "FAIL" : "ok  ");
         failures += bad;
     }
