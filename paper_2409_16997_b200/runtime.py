@@ -51,28 +51,39 @@ class AttentionPlan:
         # fp16 V codes for the two-Q-tile kernel, written by the V quantizer
         self.v16 = torch.empty(shape, dtype=torch.float16, device=dev) \
             if self.uses_pp_kernel() and d in (64, 128) and n % 128 == 0 else None
+        # V (two passes + a cluster sync per slice) runs on a side stream next to
+        # the single-pass Q/K row kernels, so HBM stays busy through V's syncs
+        self._side = torch.cuda.Stream(dev)
+        self._fork = torch.cuda.Event()
+        self._join = torch.cuda.Event()
         self.graph: Optional[torch.cuda.CUDAGraph] = None
         self._graph_io = None
 
     # ------------------------------------------------------------------
     def quantize(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
                  stream: Optional[torch.cuda.Stream] = None) -> None:
-        s = int((stream or torch.cuda.current_stream(self.device)).cuda_stream)
+        main = stream or torch.cuda.current_stream(self.device)
+        s = int(main.cuda_stream)
         L, rows, d = self.lib, self.slices * self.n, self.d
         bad = self.bad.data_ptr()
-        _lib.check(L.ifa_quantize_per_row(q.data_ptr(), rows, d, self.qc.data_ptr(),
-                                          self.sq.data_ptr(), bad, s))
-        _lib.check(L.ifa_quantize_per_row(k.data_ptr(), rows, d, self.kc.data_ptr(),
-                                          self.sk.data_ptr(), bad, s))
+        self._fork.record(main)
+        self._side.wait_event(self._fork)
+        sv = int(self._side.cuda_stream)
         if self.v16 is not None:
             _lib.check(L.ifa_quantize_per_tensor_v16(v.data_ptr(), self.slices, self.n, d,
                                                      self.vc.data_ptr(), self.v16.data_ptr(),
                                                      self.sv.data_ptr(), self.ws.data_ptr(),
-                                                     bad, s))
+                                                     bad, sv))
         else:
             _lib.check(L.ifa_quantize_per_tensor(v.data_ptr(), self.slices, self.n, d,
                                                  self.vc.data_ptr(), self.sv.data_ptr(),
-                                                 self.ws.data_ptr(), bad, s))
+                                                 self.ws.data_ptr(), bad, sv))
+        _lib.check(L.ifa_quantize_per_row(q.data_ptr(), rows, d, self.qc.data_ptr(),
+                                          self.sq.data_ptr(), bad, s))
+        _lib.check(L.ifa_quantize_per_row(k.data_ptr(), rows, d, self.kc.data_ptr(),
+                                          self.sk.data_ptr(), bad, s))
+        self._join.record(self._side)
+        main.wait_event(self._join)
 
     def attention(self, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
         s = int((stream or torch.cuda.current_stream(self.device)).cuda_stream)
