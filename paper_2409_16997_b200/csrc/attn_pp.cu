@@ -562,29 +562,64 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         alpha[r] = (j == 0 || mnew == m[r]) ? 1.0f : ex2(sq[r] * (m[r] - mnew));
                         m[r] = mnew;
                     }
-                    // codes: round(2^t) as exact fp16 integers; 6 of 8 exp2 on MUFU,
-                    // 2 on the FMA pipe.  wd[r][k] = keys (8k + 2t0, +1) of row r.
+                    // weights: 6 of 8 exp2 on MUFU, 2 on the FMA pipe.
+                    // wd[r][k] = keys (8k + 2t0, +1) of row r as fp16x2.
                     uint32_t wd[2][16];
-                    float2 ls[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
-    #pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-    #pragma unroll
-                        for (int r = 0; r < 2; ++r) {
-                            const float2 t = ffma2(make_float2(u[4 * k + 2 * r], u[4 * k + 2 * r + 1]),
-                                                   f2(sq[r]), f2(cr[r]));
-                            const float2 y = (k & kPolyMask) == kPolyMask ? exp2_poly2(t)
-                                                          : make_float2(ex2(t.x), ex2(t.y));
-                            // full-INT8: the integer code; half-INT8 / FP8: the float weight
-                            float2 c = MODE == kModeCodes ? fsub2(fadd2(y, f2(kMagic)), f2(kMagic)) : y;
-                            if (dmask) {  // masked keys weigh 0 (also when sQ == 0)
-                                const int32_t key = 8 * k + 2 * static_cast<int32_t>(t0);
-                                if (key > kmax[r]) c.x = 0.0f;
-                                if (key + 1 > kmax[r]) c.y = 0.0f;
+                    float lsum[2];
+                    if constexpr (MODE == kModeCodes) {
+                        // full-INT8: y + 1.5*2^23 has the code round(y) in its low
+                        // bits; its low 16 bits read as fp16 are the subnormal
+                        // code * 2^-24, exact, so one PRMT packs two codes (P.V
+                        // then accumulates 2^-24 * the integer P.V, undone in the
+                        // epilogue).  Row sums add the packed words as integers:
+                        // <= 16 * 127 per half, no carry between the halves.
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) {
+#pragma unroll
+                            for (int r = 0; r < 2; ++r) {
+                                const float2 t = ffma2(make_float2(u[4 * k + 2 * r], u[4 * k + 2 * r + 1]),
+                                                       f2(sq[r]), f2(cr[r]));
+                                const float2 y = (k & kPolyMask) == kPolyMask ? exp2_poly2(t)
+                                                              : make_float2(ex2(t.x), ex2(t.y));
+                                float2 c = fadd2(y, f2(kMagic));
+                                if (dmask) {  // masked keys are code 0 (also when sQ == 0)
+                                    const int32_t key = 8 * k + 2 * static_cast<int32_t>(t0);
+                                    if (key > kmax[r]) c.x = kMagic;
+                                    if (key + 1 > kmax[r]) c.y = kMagic;
+                                }
+                                wd[r][k] = prmt(__float_as_uint(c.x), __float_as_uint(c.y), 0x5410u);
                             }
-                            ls[r] = fadd2(ls[r], c);
-                            const __half2 h = __floats2half2_rn(c.x, c.y);
-                            wd[r][k] = *reinterpret_cast<const uint32_t*>(&h);
                         }
+#pragma unroll
+                        for (int r = 0; r < 2; ++r) {
+                            uint32_t acc = 0;
+#pragma unroll
+                            for (int k = 0; k < 16; k += 2) acc += wd[r][k] + wd[r][k + 1];
+                            lsum[r] = static_cast<float>(static_cast<int32_t>((acc & 0xffffu) + (acc >> 16)));
+                        }
+                    } else {
+                        // half-INT8 / FP8: the float weights, rounded to fp16
+                        float2 ls[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) {
+#pragma unroll
+                            for (int r = 0; r < 2; ++r) {
+                                const float2 t = ffma2(make_float2(u[4 * k + 2 * r], u[4 * k + 2 * r + 1]),
+                                                       f2(sq[r]), f2(cr[r]));
+                                float2 c = (k & kPolyMask) == kPolyMask ? exp2_poly2(t)
+                                                         : make_float2(ex2(t.x), ex2(t.y));
+                                if (dmask) {  // masked keys weigh 0
+                                    const int32_t key = 8 * k + 2 * static_cast<int32_t>(t0);
+                                    if (key > kmax[r]) c.x = 0.0f;
+                                    if (key + 1 > kmax[r]) c.y = 0.0f;
+                                }
+                                ls[r] = fadd2(ls[r], c);
+                                const __half2 h = __floats2half2_rn(c.x, c.y);
+                                wd[r][k] = *reinterpret_cast<const uint32_t*>(&h);
+                            }
+                        }
+#pragma unroll
+                        for (int r = 0; r < 2; ++r) lsum[r] = ls[r].x + ls[r].y;
                     }
                     // P.V(j-1) done: the P buffer is free and O(j-1) is final
                     if (tc > 0) bar_wait(bp_empty, (tc - 1) & 1);
@@ -628,7 +663,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     if (lane == 0) bar_arrive(bp_full);
 
 #pragma unroll
-                    for (int r = 0; r < 2; ++r) l[r] = __fmaf_rn(l[r], alpha[r], ls[r].x + ls[r].y);
+                    for (int r = 0; r < 2; ++r) l[r] = __fmaf_rn(l[r], alpha[r], lsum[r]);
                 };
                 if constexpr (causal || RAGGED) {
                     if ((causal && j == diag) || (RAGGED && (j + 1) * BN > n))
@@ -674,8 +709,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         const int col = 32 * c + 8 * k + 2 * static_cast<int>(t0);
-                        const float2 v = make_float2(__uint_as_float(o[4 * k + 2 * r]) * f[r],
-                                                     __uint_as_float(o[4 * k + 2 * r + 1]) * f[r]);
+                        // full-INT8: O holds 2^-24 * the integer P.V (exact rescale)
+                        constexpr float os = MODE == kModeCodes ? 16777216.0f : 1.0f;
+                        const float2 v = make_float2(__uint_as_float(o[4 * k + 2 * r]) * os * f[r],
+                                                     __uint_as_float(o[4 * k + 2 * r + 1]) * os * f[r]);
                         if (col + 1 < p.d)
                             __stcs(reinterpret_cast<float2*>(orow + col), v);
                         else if (col < p.d)
