@@ -69,6 +69,9 @@ constexpr float kLog2e = 1.4426950408889634f;
 // unit nearly keeps up: C2 1.029 ms at 15 vs 1.034 at 16 and 1.045 at 7
 // (1.232 at 3 before the P stores were conflict-free).
 constexpr int kPolyMask = IFA_PP_POLY_MASK;
+#ifndef IFA_PP_EARLY_P
+#define IFA_PP_EARLY_P 1
+#endif
 
 template <int D>
 struct alignas(1024) Smem {
@@ -566,13 +569,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     // wd[r][k] = keys (8k + 2t0, +1) of row r as fp16x2.
                     uint32_t wd[2][16];
                     float lsum[2];
+                    // words 4i..4i+3 of row r = pairs k = 4i..4i+3: atom i >> 1,
+                    // chunk 2 t0 + (i & 1)
+                    auto store_p = [&](int r, int i, const uint32_t (&w)[2][16]) {
+                        const uint32_t chunk = (2 * t0 + (i & 1)) ^ sw;
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                         p_row[r] + (i >> 1) * (BM * 128) + chunk * 16),
+                                     "r"(w[r][4 * i]), "r"(w[r][4 * i + 1]),
+                                     "r"(w[r][4 * i + 2]), "r"(w[r][4 * i + 3])
+                                     : "memory");
+                    };
+                    constexpr bool early_p = IFA_PP_EARLY_P && MODE == kModeCodes;
                     if constexpr (MODE == kModeCodes) {
+                        if constexpr (early_p) {
+                            // P.V(j-1) has long finished by now: P is stored as it is made
+                            if (tc > 0) bar_wait(bp_empty, (tc - 1) & 1);
+                            tc_fence_after();
+                        }
                         // full-INT8: y + 1.5*2^23 has the code round(y) in its low
                         // bits; its low 16 bits read as fp16 are the subnormal
                         // code * 2^-24, exact, so one PRMT packs two codes (P.V
                         // then accumulates 2^-24 * the integer P.V, undone in the
                         // epilogue).  Row sums add the packed words as integers:
                         // <= 16 * 127 per half, no carry between the halves.
+                        uint32_t acc[2] = {0u, 0u};
 #pragma unroll
                         for (int k = 0; k < 16; ++k) {
 #pragma unroll
@@ -588,15 +608,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                     if (key + 1 > kmax[r]) c.y = kMagic;
                                 }
                                 wd[r][k] = prmt(__float_as_uint(c.x), __float_as_uint(c.y), 0x5410u);
+                                if (k & 1) acc[r] += wd[r][k - 1] + wd[r][k];
+                            }
+                            if (early_p && (k & 3) == 3) {
+                                store_p(0, k >> 2, wd);
+                                store_p(1, k >> 2, wd);
                             }
                         }
 #pragma unroll
-                        for (int r = 0; r < 2; ++r) {
-                            uint32_t acc = 0;
-#pragma unroll
-                            for (int k = 0; k < 16; k += 2) acc += wd[r][k] + wd[r][k + 1];
-                            lsum[r] = static_cast<float>(static_cast<int32_t>((acc & 0xffffu) + (acc >> 16)));
-                        }
+                        for (int r = 0; r < 2; ++r)
+                            lsum[r] = static_cast<float>(static_cast<int32_t>((acc[r] & 0xffffu) + (acc[r] >> 16)));
                     } else {
                         // half-INT8 / FP8: the float weights, rounded to fp16
                         float2 ls[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
@@ -622,8 +643,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         for (int r = 0; r < 2; ++r) lsum[r] = ls[r].x + ls[r].y;
                     }
                     // P.V(j-1) done: the P buffer is free and O(j-1) is final
-                    if (tc > 0) bar_wait(bp_empty, (tc - 1) & 1);
-                    tc_fence_after();
+                    if constexpr (!early_p) {
+                        if (tc > 0) bar_wait(bp_empty, (tc - 1) & 1);
+                        tc_fence_after();
+                    }
                     const bool need = j > 0 && (alpha[0] != 1.0f || alpha[1] != 1.0f);
                     if (__any_sync(0xffffffffu, need)) {
     #pragma unroll
@@ -645,18 +668,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         }
                         tmem_wait_st();
                     }
-    #pragma unroll
-                    for (int r = 0; r < 2; ++r)
-    #pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            // words 4i..4i+3 = pairs k = 4i..4i+3: atom i >> 1, chunk 2 t0 + (i & 1)
-                            const uint32_t chunk = (2 * t0 + (i & 1)) ^ sw;
-                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
-                                             p_row[r] + (i >> 1) * (BM * 128) + chunk * 16),
-                                         "r"(wd[r][4 * i]), "r"(wd[r][4 * i + 1]),
-                                         "r"(wd[r][4 * i + 2]), "r"(wd[r][4 * i + 3])
-                                         : "memory");
-                        }
+                    if constexpr (!early_p) {
+#pragma unroll
+                        for (int r = 0; r < 2; ++r)
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) store_p(r, i, wd);
+                    }
                     fence_proxy_async_shared();  // P is read by the tensor core
                     tc_fence_before();
                     __syncwarp();
