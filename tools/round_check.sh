@@ -16,6 +16,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-extras > $OUT/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:int_flash -s 2 -c 1 \
   -o $OUT/attn_full python bench.py --steps 1 --warmup 3 --no-extras > $OUT/ncu_full.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k "regex:int_flash_pp_kernel<128, 0, 1>" -s 2 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+  -k "regex:pp_kernel<.int.128, .bool.0, .int.1" -s 2 -c 1 \
   -o $OUT/half_full python bench.py --steps 3 --warmup 3 > $OUT/ncu_half.log 2>&1
 echo done > $OUT/DONE
