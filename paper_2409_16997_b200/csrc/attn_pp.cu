@@ -579,13 +579,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                      "r"(w[r][4 * i + 2]), "r"(w[r][4 * i + 3])
                                      : "memory");
                     };
-                    constexpr bool early_p = IFA_PP_EARLY_P && MODE == kModeCodes;
+                    constexpr bool early_p = IFA_PP_EARLY_P;
+                    if constexpr (early_p) {
+                        // P.V(j-1) has long finished by now: P is stored as it is made
+                        if (tc > 0) bar_wait(bp_empty, (tc - 1) & 1);
+                        tc_fence_after();
+                    }
                     if constexpr (MODE == kModeCodes) {
-                        if constexpr (early_p) {
-                            // P.V(j-1) has long finished by now: P is stored as it is made
-                            if (tc > 0) bar_wait(bp_empty, (tc - 1) & 1);
-                            tc_fence_after();
-                        }
                         // full-INT8: y + 1.5*2^23 has the code round(y) in its low
                         // bits; its low 16 bits read as fp16 are the subnormal
                         // code * 2^-24, exact, so one PRMT packs two codes (P.V
@@ -637,6 +637,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                 ls[r] = fadd2(ls[r], c);
                                 const __half2 h = __floats2half2_rn(c.x, c.y);
                                 wd[r][k] = *reinterpret_cast<const uint32_t*>(&h);
+                            }
+                            if (early_p && (k & 3) == 3) {
+                                store_p(0, k >> 2, wd);
+                                store_p(1, k >> 2, wd);
                             }
                         }
 #pragma unroll
