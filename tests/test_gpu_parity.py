@@ -366,3 +366,42 @@ def test_fast_mode_pp_batched_slices(ifa, oracle):
                                               vc[bi, hi], float(vs[bi, hi]), 128, 128)
             mre, mx, bound = _fast_close(got[bi, hi], want, vc[bi, hi], vs[bi, hi])
             assert mre <= FAST_MRE and mx <= bound, (bi, hi, mre, mx)
+
+
+@pytest.mark.parametrize("case", ["zero_q_rows", "v_tiny", "v_huge", "rising_max", "one_hot"])
+@pytest.mark.parametrize("causal", [False, True])
+def test_fast_mode_pp_code_edges(ifa, oracle, case, causal):
+    """Edge cases of the two-Q-tile kernel's P encoding (codes as fp16
+    subnormals code * 2^-24, O rescaled by 2^24 in the epilogue, integer row
+    sums): sQ == 0 rows (every code 127), V scales near the f32 range ends
+    (the 2^24 factor must neither overflow nor flush), a running max that keeps
+    rising tile after tile (O rescaled by tiny alphas every tile), and one
+    dominant key per row (codes mostly 0)."""
+    n, d = 512, 128
+    rng = np.random.default_rng(17)
+    q = rng.standard_normal((n, d)).astype(np.float32)
+    k = rng.standard_normal((n, d)).astype(np.float32)
+    v = rng.standard_normal((n, d)).astype(np.float32)
+    if case == "zero_q_rows":
+        q[::5] = 0.0
+    elif case == "v_tiny":
+        v *= np.float32(1e-30)
+    elif case == "v_huge":
+        v *= np.float32(1e30)
+    elif case == "rising_max":
+        k *= np.linspace(0.1, 6.0, n, dtype=np.float32)[:, None]
+    elif case == "one_hot":
+        k = np.tile(q[:1], (n, 1)) * np.float32(0.01)
+        k[::97] = q[0] * np.float32(8.0)
+    qc, qs = oracle.quantize_per_row(q)
+    kc, ks = oracle.quantize_per_row(k)
+    vc, vs = oracle.quantize_per_tensor(v)
+    want = oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, 128, flags=2 if causal else 0)
+    inputs = ifa.QuantizedAttentionInputs(
+        ifa.QuantizedRows(_dev(qc), _dev(qs)), ifa.QuantizedRows(_dev(kc), _dev(ks)),
+        ifa.QuantizedTensor(_dev(vc), _dev(np.asarray(vs, np.float32))))
+    got = ifa.int_flash_attention(inputs, ifa.AttentionConfig(
+        ifa.BlockSpec(64, 128), causal=causal, fast=True)).cpu().numpy()
+    assert np.isfinite(got).all()
+    mre, mx, bound = _fast_close(got, want, vc, vs)
+    assert mre <= FAST_MRE and mx <= bound, (case, mre, mx, bound)
