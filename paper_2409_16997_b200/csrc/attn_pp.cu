@@ -62,12 +62,12 @@ constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
 constexpr float kLog2_127 = 6.9886846867721655f;
 constexpr float kLog2e = 1.4426950408889634f;
 #ifndef IFA_PP_POLY_MASK
-#define IFA_PP_POLY_MASK 15
+#define IFA_PP_POLY_MASK 16
 #endif
 // key pairs k with (k & mask) == mask take exp2 on the FMA pipe (3: 1 in 4,
 // 15: 1 in 16, 16: none).  With four math warps per sub-partition the MUFU
-// unit nearly keeps up: C2 1.029 ms at 15 vs 1.034 at 16 and 1.045 at 7
-// (1.232 at 3 before the P stores were conflict-free).
+// unit keeps up: C2 0.982 ms at 16 vs 0.989 at 15 and 0.985 at 7 (with the
+// groups de-phased; 1.029 at 15 vs 1.034 at 16 before).
 constexpr int kPolyMask = IFA_PP_POLY_MASK;
 #ifndef IFA_PP_G1_DELAY_NS
 #define IFA_PP_G1_DELAY_NS 1000
