@@ -48,8 +48,14 @@ using namespace ptx;
 
 constexpr int BM = 128;
 constexpr int BN = 128;
-constexpr int KST = 3;  // K tiles (+ K scales) in flight
-constexpr int VST = 2;  // fp16 V tiles in flight
+#ifndef IFA_PP_KST
+#define IFA_PP_KST 2
+#endif
+constexpr int KST = IFA_PP_KST;  // K tiles (+ K scales) in flight
+#ifndef IFA_PP_VST
+#define IFA_PP_VST 2
+#endif
+constexpr int VST = IFA_PP_VST;  // fp16 V tiles in flight
 constexpr int CTRL_WARPS = 4;
 constexpr int GROUP_WARPS = 8;
 constexpr int NUM_THREADS = 32 * (CTRL_WARPS + 2 * GROUP_WARPS);
