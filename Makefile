@@ -10,7 +10,7 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 PKG := paper_2409_16997_b200
 CSRC := $(PKG)/csrc
 LIB := $(PKG)/lib/libifa_b200.so
-SRCS := $(CSRC)/abi.cu $(CSRC)/host_abi.cu $(CSRC)/attn.cu $(CSRC)/attn_half.cu $(CSRC)/attn_pp.cu $(CSRC)/quant.cu $(CSRC)/code_bounds.cpp \
+SRCS := $(CSRC)/abi.cu $(CSRC)/host_abi.cu $(CSRC)/attn.cu $(CSRC)/attn_half.cu $(CSRC)/attn_pp.cu $(CSRC)/attn_ws.cu $(CSRC)/quant.cu $(CSRC)/code_bounds.cpp \
         $(CSRC)/tensor_io.cpp
 HDRS := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/ifa_b200.h
 NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=false \

@@ -964,7 +964,12 @@ static cudaError_t launch(const AttnArgs& a, const uint16_t* v16_given, cudaStre
         p.o = o_even;
         p.o_pitch = static_cast<int32_t>(a.d + 1);
     }
-    e = run<D, kModeCodes>(a.q, a.k, v16, p, a.pitch, (a.flags & IFA_FLAG_CAUSAL) != 0, stream);
+    if (int_flash_ws_enabled() || a.dump != nullptr)
+        e = launch_int_flash_ws(a.q, a.sq, a.k, a.sk, reinterpret_cast<const uint16_t*>(v16), a.sv,
+                                p.o, a.slices, a.n, a.d, a.pitch, p.o_pitch, a.flags, a.dump,
+                                stream);
+    else
+        e = run<D, kModeCodes>(a.q, a.k, v16, p, a.pitch, (a.flags & IFA_FLAG_CAUSAL) != 0, stream);
     if (o_even) {
         if (e == cudaSuccess)
             e = cudaMemcpy2DAsync(a.o, sizeof(float) * a.d, o_even, sizeof(float) * (a.d + 1),

@@ -24,6 +24,13 @@ cudaError_t launch_quantize_per_tensor(const float* x, int64_t slices, int64_t r
                                        uint32_t* amax_ws, int64_t* bad, cudaStream_t stream,
                                        uint16_t* codes_f16 = nullptr);
 
+// Optional debug outputs of the tolerance-mode kernel (attn_ws.cu):
+// s = [slices][n][n] int32 S tiles, p = [slices][n][n] uint8 P codes.
+struct AttnDump {
+    int32_t* s = nullptr;
+    uint8_t* p = nullptr;
+};
+
 struct AttnArgs {
     const int8_t* q;
     const float* sq;
@@ -39,6 +46,7 @@ struct AttnArgs {
     int64_t pitch;   // row pitch (elements) of the q/k/v code buffers, % 16 == 0
     int64_t bc;
     uint32_t flags;
+    const AttnDump* dump = nullptr;  // tolerance-mode kernel only
 };
 
 // q/k/v rows have pitch `pitch` >= d with pitch % 16 == 0 (the C-ABI layer
@@ -51,6 +59,16 @@ bool int_flash_pp_eligible(const AttnArgs& a);
 // v16: [slices][n][D] fp16 copy of the V codes (D = 64 for d <= 64, else
 // 128), or null to convert a.v internally.
 cudaError_t launch_int_flash_pp(const AttnArgs& a, const uint16_t* v16, cudaStream_t stream);
+// attn_ws.cu: the full-INT8 tolerance-mode kernel with one softmax thread
+// per row (IFA_B200_WS=1 selects it for int_flash_pp_eligible calls, and it
+// serves the S / P-code dumps).  v16 = [slices][n_pad][D] fp16 V codes (n_pad = n rounded up
+// to 128, zero rows past n), o rows of o_pitch floats.
+bool int_flash_ws_enabled();
+cudaError_t launch_int_flash_ws(const int8_t* q, const float* sq, const int8_t* k,
+                                const float* sk, const uint16_t* v16, const float* sv, float* o,
+                                int64_t slices, int64_t n, int64_t d, int64_t pitch,
+                                int64_t o_pitch, uint32_t flags, const AttnDump* dump,
+                                cudaStream_t stream);
 // The same two-Q-tile pipeline for the float-weight variants (§8(f) f1, f3):
 // n % 128 == 0, d in {64, 128}, non-causal; v16 = fp16 V [slices][n][d].
 bool float_weights_pp_eligible(int64_t n, int64_t d);

@@ -76,9 +76,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void bar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// One non-blocking test of the phase (no suspend hint).
+__device__ __forceinline__ bool bar_try(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+#ifndef IFA_WAIT_HINT
+#define IFA_WAIT_HINT 1
+#endif
 __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
     uint32_t ok;
     do {
+#if IFA_WAIT_HINT
         asm volatile(
             "{\n\t.reg .pred P;\n\t"
             "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2, 10000000;\n\t"
@@ -86,6 +103,15 @@ __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
             : "=r"(ok)
             : "r"(bar), "r"(parity)
             : "memory");
+#else
+        asm volatile(
+            "{\n\t.reg .pred P;\n\t"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P;\n\t}\n"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+#endif
     } while (!ok);
 }
 

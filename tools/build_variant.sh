@@ -8,4 +8,4 @@ mkdir -p build/$NAME
 C=paper_2409_16997_b200/csrc
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=false \
   -Xcompiler -fPIC --expt-relaxed-constexpr "$@" -shared -o build/$NAME/libifa_b200.so \
-  $C/abi.cu $C/host_abi.cu $C/attn.cu $C/attn_half.cu $C/attn_pp.cu $C/quant.cu $C/code_bounds.cpp $C/tensor_io.cpp -lcuda
+  $C/abi.cu $C/host_abi.cu $C/attn.cu $C/attn_half.cu $C/attn_pp.cu $C/attn_ws.cu $C/quant.cu $C/code_bounds.cpp $C/tensor_io.cpp -lcuda

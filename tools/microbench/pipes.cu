@@ -33,6 +33,11 @@ __global__ void bench(float* out, long long* cyc, int seed) {
             if (OP == 7) { asm volatile("add.s32 %0, %0, 1262485504;" : "+r"(iv[c])); }
             if (OP == 8) { asm volatile("add.rn.f32 %0, %0, 0f3F800000;" : "+f"(f[c])); }
             if (OP == 9) { float r; asm volatile("cvt.rni.f32.f32 %0, %1;" : "=f"(r) : "f"(f[c])); f[c] = r + 0.5f; }
+            if (OP == 11) { asm volatile("mad.lo.s32 %0, %0, 1, 1262485504;" : "+r"(iv[c])); }
+            if (OP == 12) { float2 q = p[c]; asm volatile("{.reg .b64 ra, rb, rd;\n mov.b64 ra, {%0,%1};\n mov.b64 rb, {%2,%3};\n mul.rn.f32x2 rd, ra, rb;\n mov.b64 {%0,%1}, rd;}" : "+f"(q.x), "+f"(q.y) : "f"(1.0001f), "f"(0.9999f)); p[c] = q; }
+            if (OP == 13) { float r; asm volatile("cvt.rn.f32.s32 %0, %1;" : "=f"(r) : "r"(iv[c])); float r2; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(r2) : "f"(f[c])); f[c] = r2; iv[c] = __float_as_int(r) ^ c; }
+            if (OP == 14) { unsigned r; asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(f[c]), "f"(f[(c+1)%CHAINS])); iv[c] ^= r; f[c] += 1.0f; }
+            if (OP == 15) { unsigned h = 0x3c003c00u ^ (iv[c] & 0x00ff00ff); unsigned r; asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(h)); iv[c] = r; }
             if (OP == 10) { asm volatile("setp.gt.f32 %%p1, %0, 0f3EFFF000; selp.b32 %1, 1, %1, %%p1;" : "+f"(f[c]), "+r"(iv[c])); }
         }
         }
@@ -46,7 +51,7 @@ __global__ void bench(float* out, long long* cyc, int seed) {
 int main() {
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     float* out; long long* cyc; cudaMalloc(&out, sms * 1024 * 4); cudaMalloc(&cyc, sms * 8);
-    const char* names[] = {"I2F(cvt.rn.f32.s32)", "FADD2", "FFMA2", "MUFU.EX2", "PRMT", "IDP4A", "FMNMX3", "IADD", "FADD", "FRND", "FSETP+SEL"};
+    const char* names[] = {"I2F(cvt.rn.f32.s32)", "FADD2", "FFMA2", "MUFU.EX2", "PRMT", "IDP4A", "FMNMX3", "IADD", "FADD", "FRND", "FSETP+SEL", "IMAD(x*1+c)", "FMUL2", "I2F+MUFU mix", "F2F.F16x2", "EX2.F16x2"};
     auto run = [&](auto kern, int op) {
         kern<<<sms, 1024>>>(out, cyc, 3); cudaDeviceSynchronize();
         kern<<<sms, 1024>>>(out, cyc, 3); cudaDeviceSynchronize();
@@ -56,5 +61,6 @@ int main() {
     };
     run(bench<0>, 0); run(bench<1>, 1); run(bench<2>, 2); run(bench<3>, 3); run(bench<4>, 4); run(bench<5>, 5);
     run(bench<6>, 6); run(bench<7>, 7); run(bench<8>, 8); run(bench<9>, 9); run(bench<10>, 10);
+    run(bench<11>, 11); run(bench<12>, 12); run(bench<13>, 13); run(bench<14>, 14); run(bench<15>, 15);
     return 0;
 }
