@@ -24,9 +24,17 @@ all: $(LIB) $(CLI) oracle
 $(CLI): tools/ifa_b200_cli.cpp include/ifa_b200.h $(LIB)
 	g++ -O2 -std=c++17 -Iinclude -o $@ $< -L$(PKG)/lib -lifa_b200 -Wl,-rpath,'$$ORIGIN'
 
-$(LIB): $(SRCS) $(HDRS)
-	@mkdir -p $(PKG)/lib
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) -lcuda 2> $(PKG)/lib/ptxas.log || (cat $(PKG)/lib/ptxas.log; exit 1)
+OBJDIR := $(PKG)/lib/obj
+OBJS := $(patsubst $(CSRC)/%,$(OBJDIR)/%.o,$(SRCS))
+
+# one object per translation unit, so `make -j` compiles the kernels in parallel
+$(OBJDIR)/%.o: $(CSRC)/% $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $@.ptxas.log || (cat $@.ptxas.log; exit 1)
+
+$(LIB): $(OBJS)
+	$(NVCC) -gencode arch=compute_100a,code=sm_100a -shared -o $@ $(OBJS) -lcuda
+	@cat $(OBJDIR)/*.ptxas.log > $(PKG)/lib/ptxas.log
 
 oracle:
 	$(MAKE) -s -C oracle all

@@ -103,6 +103,29 @@ int ifa_int_flash_fwd(const int8_t* q, const float* sq, const int8_t* k, const f
                       int64_t d, int64_t br, int64_t bc, uint32_t flags,
                       ifa_pcode_audit* audit, void* stream);
 
+/* ---- int32 S / P-code dump (north_star: "int32 S tiles bit-exact") --------
+ * ifa_int_flash_fwd_dump: ifa_int_flash_fwd in tolerance mode (flags must
+ *   hold IFA_FLAG_FAST; Bc = 128, or Bc >= n <= 128) through a separate
+ *   instantiation of the full-INT8 tolerance kernel that also writes
+ *     s_out   [slices][n][n] int32: S = Q.K^T of every KV tile the kernel
+ *             computes, read back from the tcgen05 kind::i8 accumulator in
+ *             TMEM -- the reference's int_gemm_nt_strided
+ *             (attention.cpp:275-276 -> gemm.cpp:32-46, oracle
+ *             oracles.cpp:28-43), bit-exact;
+ *     p_codes [slices][n][n] uint8: the P codes round(127 exp(s - m_new))
+ *             the kernel fed to P.V (attention.cpp:299-312); in tolerance
+ *             mode a code may differ from the reference's by one where
+ *             127 exp(.) lies within the exp2 estimate's error of .5.
+ *   Either output may be NULL (not both).  With IFA_FLAG_CAUSAL only the KV
+ *   tiles at or below the diagonal are written (entries above the diagonal
+ *   inside the diagonal tile are S as computed, their P code 0).  O is
+ *   written as by ifa_int_flash_fwd.  n <= 65536. */
+#define IFA_FLAG_DUMP_S 8u
+int ifa_int_flash_fwd_dump(const int8_t* q, const float* sq, const int8_t* k, const float* sk,
+                           const int8_t* v, const float* sv, float* o, int64_t slices, int64_t n,
+                           int64_t d, int64_t br, int64_t bc, uint32_t flags, int32_t* s_out,
+                           uint8_t* p_codes, void* stream);
+
 /* ---- fp16 V codes for the two-Q-tile tolerance kernel --------------------
  * ifa_quantize_per_tensor_v16: ifa_quantize_per_tensor that also writes the
  *   V codes as fp16 (codes_f16, same [slices][rows][cols] layout, exact),
@@ -176,6 +199,23 @@ int ifa_int_flash_fwd_host(const int8_t* q, const float* sq, const int8_t* k, co
                            const int8_t* v, const float* sv, float* o, int64_t slices,
                            int64_t n, int64_t d, int64_t br, int64_t bc, uint32_t flags,
                            ifa_pcode_audit* audit, void* stream);
+
+/* The reference's full-INT8 evaluation step (eval.cpp:98-102, run_variant):
+ * quantize_per_row(Q), quantize_per_row(K), quantize_per_tensor(V) per
+ * slice, then int_flash_attention -- from f32 HOST Q, K, V [slices][n][d]
+ * to f32 HOST O.  flags as ifa_int_flash_fwd (IFA_FLAG_FAST selects the
+ * tolerance kernel).  Non-finite input: IFA_EINVAL "full_int8_attention:
+ * <q|k|v>: non-finite input at index <flat index>" (quant.cpp:14-22).
+ *
+ * Both host-buffer attention entry points run as a chunked pipeline over
+ * the slices: three streams overlap the host->device copy of one chunk, the
+ * kernels of the previous one and the device->host copy of the one before
+ * (PCIe is full duplex).  Pinned caller memory (cudaMallocHost /
+ * cudaHostRegister) is copied by DMA directly; pageable memory is staged
+ * through pinned buffers with multi-threaded memcpy. */
+int ifa_full_int8_attention_host(const float* q, const float* k, const float* v, float* o,
+                                 int64_t slices, int64_t n, int64_t d, int64_t br, int64_t bc,
+                                 uint32_t flags, void* stream);
 
 /* Host-buffer forms of the §8(f) variants (what include/ifa_b200.hpp's
  * ifa_gpu::half_int8_attention / fp8_emulated_attention call):

@@ -82,6 +82,46 @@ inline ifa::FloatMatrix int_flash_attention(const ifa::QuantizedAttentionInputs&
     return out;
 }
 
+/// The same drop-in on the bench-default tolerance kernel (IFA_FLAG_FAST,
+/// csrc/attn_pp.cu / attn_ws.cu): same signature as ifa::IntFlashFn
+/// (verify.hpp:15-16), so `opts.int_flash = ifa_gpu::int_flash_attention_fast`
+/// runs the reference's suites and callers on it.  int8 codes, scales and S
+/// are exact; O is within the tolerance include/ifa_b200.h states.  With an
+/// audit requested the exact kernel runs (the audit is defined on exact codes).
+inline ifa::FloatMatrix int_flash_attention_fast(const ifa::QuantizedAttentionInputs& inputs,
+                                                 const ifa::AttentionConfig& cfg,
+                                                 ifa::PCodeAudit* audit = nullptr) {
+    if (audit) return ifa_gpu::int_flash_attention(inputs, cfg, audit);
+    inputs.validate();
+    cfg.validate();
+    const int64_t n = inputs.q.values.rows(), d = inputs.q.values.cols();
+    ifa::FloatMatrix out(n, d);
+    const uint32_t flags = IFA_FLAG_FAST | (cfg.apply_sqrt_d_scaling ? IFA_FLAG_SQRT_D : 0u);
+    check(ifa_int_flash_fwd_host(inputs.q.values.data(), inputs.q.scales.data(),
+                                 inputs.k.values.data(), inputs.k.scales.data(),
+                                 inputs.v.values.data(), &inputs.v.scale, out.data(), 1, n, d,
+                                 cfg.blocks.Br, cfg.blocks.Bc, flags, nullptr, nullptr));
+    return out;
+}
+
+/// eval.cpp:98-102's full-INT8 step (quantize Q, K per row and V per tensor,
+/// then int_flash_attention) from float matrices, on the GPU in one call.
+inline ifa::FloatMatrix full_int8_attention(const ifa::FloatMatrix& q, const ifa::FloatMatrix& k,
+                                            const ifa::FloatMatrix& v,
+                                            const ifa::AttentionConfig& cfg, bool fast = true) {
+    const int64_t n = q.rows(), d = q.cols();
+    if (k.rows() != n || k.cols() != d || v.rows() != n || v.cols() != d)
+        throw std::invalid_argument("quantized attention inputs: q, k, v must all be " +
+                                    std::to_string(n) + "x" + std::to_string(d));
+    cfg.validate();
+    ifa::FloatMatrix out(n, d);
+    const uint32_t flags = (fast ? IFA_FLAG_FAST : 0u) |
+                           (cfg.apply_sqrt_d_scaling ? IFA_FLAG_SQRT_D : 0u);
+    check(ifa_full_int8_attention_host(q.data(), k.data(), v.data(), out.data(), 1, n, d,
+                                       cfg.blocks.Br, cfg.blocks.Bc, flags, nullptr));
+    return out;
+}
+
 /// Drop-in for ifa::half_int8_attention (attention.hpp:93-96,
 /// attention.cpp:359-399): same signature and exceptions; O within the
 /// tolerance include/ifa_b200.h states (fp16 weights on the tensor core).

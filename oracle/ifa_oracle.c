@@ -246,10 +246,42 @@ void ifa_or_int_gemm_nt(const int8_t *a, const int8_t *b, int64_t m, int64_t n, 
 /* ------------------------------------------------------------------ */
 /* int_flash_attention (attention.cpp:235-357) + causal extension       */
 /* ------------------------------------------------------------------ */
+static int int_flash_impl(const int8_t *q, const float *sq, const int8_t *k, const float *sk,
+                          const int8_t *v, float sv, int64_t n, int64_t d, int64_t br_cfg,
+                          int64_t bc_cfg, uint32_t flags, float *out, ifa_or_audit *audit,
+                          uint8_t *pdump, int64_t row_begin, int64_t row_end);
+
 int ifa_or_int_flash_attention(const int8_t *q, const float *sq, const int8_t *k,
                                const float *sk, const int8_t *v, float sv, int64_t n,
                                int64_t d, int64_t br_cfg, int64_t bc_cfg, uint32_t flags,
                                float *out, ifa_or_audit *audit) {
+    return int_flash_impl(q, sq, k, sk, v, sv, n, d, br_cfg, bc_cfg, flags, out, audit, NULL, 0,
+                          n);
+}
+
+int ifa_or_int_flash_attention_rows(const int8_t *q, const float *sq, const int8_t *k,
+                                    const float *sk, const int8_t *v, float sv, int64_t n,
+                                    int64_t d, int64_t br_cfg, int64_t bc_cfg, uint32_t flags,
+                                    int64_t row_begin, int64_t row_end, float *out) {
+    if (br_cfg < 1 || row_begin < 0 || row_begin % br_cfg != 0 || row_end > n ||
+        row_end < row_begin)
+        return -1;
+    return int_flash_impl(q, sq, k, sk, v, sv, n, d, br_cfg, bc_cfg, flags, out, NULL, NULL,
+                          row_begin, row_end);
+}
+
+int ifa_or_int_flash_attention_pcodes(const int8_t *q, const float *sq, const int8_t *k,
+                                      const float *sk, const int8_t *v, float sv, int64_t n,
+                                      int64_t d, int64_t br_cfg, int64_t bc_cfg, uint32_t flags,
+                                      float *out, uint8_t *pcodes) {
+    return int_flash_impl(q, sq, k, sk, v, sv, n, d, br_cfg, bc_cfg, flags, out, NULL, pcodes, 0,
+                          n);
+}
+
+static int int_flash_impl(const int8_t *q, const float *sq, const int8_t *k, const float *sk,
+                          const int8_t *v, float sv, int64_t n, int64_t d, int64_t br_cfg,
+                          int64_t bc_cfg, uint32_t flags, float *out, ifa_or_audit *audit,
+                          uint8_t *pdump, int64_t row_begin, int64_t row_end) {
     if (n < 1 || d < 1) return -1;                      /* attention.cpp:215-218 */
     if (!(sv >= 0.0f) || !isfinite(sv)) return -1;      /* attention.cpp:230-232 */
     if (br_cfg < 1 || bc_cfg < 1) return -1;            /* gemm.cpp:16-20 */
@@ -279,7 +311,7 @@ int ifa_or_int_flash_attention(const int8_t *q, const float *sq, const int8_t *k
     }
     int32_t code_min = 127, code_max = 0;
 
-    for (int64_t i0 = 0; i0 < n; i0 += br_cfg) { /* attention.cpp:267 */
+    for (int64_t i0 = row_begin; i0 < row_end; i0 += br_cfg) { /* attention.cpp:267 */
         const int64_t br = (br_cfg < n - i0) ? br_cfg : n - i0;
         for (int64_t r = 0; r < br; ++r) {
             m[r] = -INFINITY;
@@ -324,10 +356,12 @@ int ifa_or_int_flash_attention(const int8_t *q, const float *sq, const int8_t *k
                 for (int64_t c = 0; c < bc; ++c) {
                     if (!vrow[c]) {
                         prow[c] = 0;
+                        if (pdump) pdump[(i0 + r) * n + j0 + c] = 0;
                         continue;
                     }
                     const int32_t code = (int32_t)roundf(127.0f * expf(srow[c] - m_new));
                     prow[c] = (int8_t)code;
+                    if (pdump) pdump[(i0 + r) * n + j0 + c] = (uint8_t)code;
                     p_sum += code;
                     has_full = has_full || code == 127;
                     if (code < code_min) code_min = code;

@@ -65,6 +65,23 @@ int ifa_or_int_flash_attention(const int8_t *q, const float *sq, const int8_t *k
                                int64_t d, int64_t br, int64_t bc, uint32_t flags,
                                float *out, ifa_or_audit *audit);
 
+/* ifa_or_int_flash_attention that also records every P code it feeds to
+ * P.V (attention.cpp:299-312) into pcodes[n][n] (row i, key j of block j0;
+ * masked causal entries 0; entries never visited are left untouched). */
+int ifa_or_int_flash_attention_pcodes(const int8_t *q, const float *sq, const int8_t *k,
+                                      const float *sk, const int8_t *v, float sv, int64_t n,
+                                      int64_t d, int64_t br, int64_t bc, uint32_t flags,
+                                      float *out, uint8_t *pcodes);
+
+/* ifa_or_int_flash_attention restricted to the row blocks starting in
+ * [row_begin, row_end) (row_begin a multiple of br; row blocks are
+ * independent in the reference, attention.cpp:267): writes only those rows
+ * of out[n][d].  For spot checks of long sequences (C3 / C5). */
+int ifa_or_int_flash_attention_rows(const int8_t *q, const float *sq, const int8_t *k,
+                                    const float *sk, const int8_t *v, float sv, int64_t n,
+                                    int64_t d, int64_t br, int64_t bc, uint32_t flags,
+                                    int64_t row_begin, int64_t row_end, float *out);
+
 /* Batched form over [slices][n][d] using up to `threads` host threads
  * (one slice per task from an atomic queue).  audit may be NULL. */
 int ifa_or_int_flash_attention_batched(const int8_t *q, const float *sq, const int8_t *k,

@@ -17,6 +17,7 @@ from .api import (  # noqa: F401
     fp8_quantize_per_tensor,
     half_int8_attention,
     int_flash_attention,
+    int_flash_attention_dump,
     quantize_per_row,
     quantize_per_tensor,
     version,
@@ -26,6 +27,6 @@ from ._lib import NativeLibraryError  # noqa: F401
 __all__ = [
     "AttentionConfig", "BlockSpec", "PCodeAudit", "QuantizedAttentionInputs",
     "QuantizedRows", "QuantizedTensor", "Fp8Tensor", "fp8_emulated_attention",
-    "fp8_quantize_per_tensor", "half_int8_attention", "int_flash_attention", "quantize_per_row",
+    "fp8_quantize_per_tensor", "half_int8_attention", "int_flash_attention", "int_flash_attention_dump", "quantize_per_row",
     "quantize_per_tensor", "version", "NativeLibraryError",
 ]

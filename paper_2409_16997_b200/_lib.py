@@ -22,12 +22,14 @@ IFA_EFORMAT = 74
 FLAG_SQRT_D = 1
 FLAG_CAUSAL = 2
 FLAG_FAST = 4
+FLAG_DUMP_S = 8
 
 # Every symbol include/ifa_b200.h declares.
 EXPORTED_SYMBOLS = (
     "ifa_quantize_per_row",
     "ifa_quantize_per_tensor",
     "ifa_int_flash_fwd",
+    "ifa_int_flash_fwd_dump",
     "ifa_half_int8_fwd",
     "ifa_convert_f16",
     "ifa_quantize_per_tensor_v16",
@@ -37,6 +39,7 @@ EXPORTED_SYMBOLS = (
     "ifa_quantize_per_row_host",
     "ifa_quantize_per_tensor_host",
     "ifa_int_flash_fwd_host",
+    "ifa_full_int8_attention_host",
     "ifa_half_int8_fwd_host",
     "ifa_fp8_emulated_attention_host",
     "ifa_tensor_save",
@@ -89,6 +92,9 @@ def load() -> C.CDLL:
     lib.ifa_int_flash_fwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64,
                                       u32, vp, vp]
     lib.ifa_int_flash_fwd.restype = C.c_int
+    lib.ifa_int_flash_fwd_dump.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i64,
+                                           i64, u32, vp, vp, vp]
+    lib.ifa_int_flash_fwd_dump.restype = C.c_int
     lib.ifa_half_int8_fwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, u32, vp]
     lib.ifa_half_int8_fwd.restype = C.c_int
     lib.ifa_convert_f16.argtypes = [vp, i64, vp, vp]
@@ -110,6 +116,9 @@ def load() -> C.CDLL:
     lib.ifa_int_flash_fwd_host.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64,
                                            u32, vp, vp]
     lib.ifa_int_flash_fwd_host.restype = C.c_int
+    lib.ifa_full_int8_attention_host.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64, i64, u32,
+                                                 vp]
+    lib.ifa_full_int8_attention_host.restype = C.c_int
     lib.ifa_half_int8_fwd_host.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, u32,
                                            vp]
     lib.ifa_half_int8_fwd_host.restype = C.c_int

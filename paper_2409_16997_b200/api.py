@@ -43,9 +43,30 @@ K_MAX_INT_GEMM_DEPTH = (1 << 31) // (127 * 127)  # gemm.hpp:22 (133144)
 _INT64_MAX = (1 << 63) - 1
 
 
-def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
+def _stream_ptr(stream: Optional[torch.cuda.Stream],
+                device: Optional[torch.device] = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return int(s.cuda_stream)
+
+
+def _join(stream: Optional[torch.cuda.Stream], device: torch.device, *temps) -> None:
+    """After launching on a caller-supplied ``stream``: keep the temporaries
+    allocated on the current stream alive for ``stream`` and order the current
+    stream (where host readbacks happen) after it."""
+    if stream is None:
+        return
+    for t in temps:
+        if t is not None:
+            t.record_stream(stream)
+    torch.cuda.current_stream(device).wait_stream(stream)
+
+
+def _check_out(out: torch.Tensor, like: torch.Tensor, what: str) -> None:
+    if not isinstance(out, torch.Tensor) or out.dtype != torch.float32 or \
+            out.device != like.device or tuple(out.shape) != tuple(like.shape) or \
+            not out.is_contiguous():
+        raise ValueError(f"{what}: out must be a contiguous float32 tensor of shape "
+                         f"{tuple(like.shape)} on {like.device}")
 
 
 def _require_cuda(t: torch.Tensor, dtype: torch.dtype, what: str) -> None:
@@ -151,10 +172,12 @@ def quantize_per_row(x: torch.Tensor, *, check_finite: bool = True,
     bad = torch.full((1,), _INT64_MAX, dtype=torch.int64, device=x.device) if check_finite \
         else None
     lib = _lib.load()
-    _lib.check(lib.ifa_quantize_per_row(x.data_ptr(), rows, cols, codes.data_ptr(),
-                                        scales.data_ptr(),
-                                        bad.data_ptr() if bad is not None else None,
-                                        _stream_ptr(stream)))
+    with torch.cuda.device(x.device):
+        _lib.check(lib.ifa_quantize_per_row(x.data_ptr(), rows, cols, codes.data_ptr(),
+                                            scales.data_ptr(),
+                                            bad.data_ptr() if bad is not None else None,
+                                            _stream_ptr(stream, x.device)))
+    _join(stream, x.device, bad)
     if bad is not None:
         idx = int(bad.item())
         if idx != _INT64_MAX:
@@ -177,10 +200,12 @@ def quantize_per_tensor(x: torch.Tensor, *, check_finite: bool = True,
     bad = torch.full((1,), _INT64_MAX, dtype=torch.int64, device=x.device) if check_finite \
         else None
     lib = _lib.load()
-    _lib.check(lib.ifa_quantize_per_tensor(x.data_ptr(), slices, rows, cols, codes.data_ptr(),
-                                           scale.data_ptr(), ws.data_ptr(),
-                                           bad.data_ptr() if bad is not None else None,
-                                           _stream_ptr(stream)))
+    with torch.cuda.device(x.device):
+        _lib.check(lib.ifa_quantize_per_tensor(x.data_ptr(), slices, rows, cols,
+                                               codes.data_ptr(), scale.data_ptr(), ws.data_ptr(),
+                                               bad.data_ptr() if bad is not None else None,
+                                               _stream_ptr(stream, x.device)))
+    _join(stream, x.device, bad, ws)
     if bad is not None:
         idx = int(bad.item())
         if idx != _INT64_MAX:
@@ -207,8 +232,7 @@ def int_flash_attention(inputs: QuantizedAttentionInputs,
     if validate:
         inputs.validate()
     else:
-        if qv.dim() < 2 or qv.shape[-2] < 1 or qv.shape[-1] < 1:
-            raise ValueError("quantized attention inputs: empty q")
+        _check_shapes(inputs)
     cfg.validate()
     n, d = qv.shape[-2], qv.shape[-1]
     slices = qv.numel() // (n * d)
@@ -218,18 +242,23 @@ def int_flash_attention(inputs: QuantizedAttentionInputs,
     sv = inputs.v.scale.contiguous().reshape(-1)
     if out is None:
         out = torch.empty(qv.shape, dtype=torch.float32, device=qv.device)
+    else:
+        _check_out(out, qv, "int_flash_attention")
     flags = (_lib.FLAG_SQRT_D if cfg.apply_sqrt_d_scaling else 0) | \
         (_lib.FLAG_CAUSAL if cfg.causal else 0) | (_lib.FLAG_FAST if cfg.fast else 0)
     lib = _lib.load()
     au = None
-    sp = _stream_ptr(stream)
-    if audit is not None:
-        au = torch.empty(3, dtype=torch.int64, device=qv.device)  # 24 bytes
-        _lib.check(lib.ifa_audit_init(au.data_ptr(), sp))
-    _lib.check(lib.ifa_int_flash_fwd(q.data_ptr(), sq.data_ptr(), k.data_ptr(), sk.data_ptr(),
-                                     v.data_ptr(), sv.data_ptr(), out.data_ptr(), slices, n, d,
-                                     cfg.blocks.Br, cfg.blocks.Bc, flags,
-                                     au.data_ptr() if au is not None else None, sp))
+    with torch.cuda.device(qv.device):
+        sp = _stream_ptr(stream, qv.device)
+        if audit is not None:
+            au = torch.empty(3, dtype=torch.int64, device=qv.device)  # 24 bytes
+            _lib.check(lib.ifa_audit_init(au.data_ptr(), sp))
+        _lib.check(lib.ifa_int_flash_fwd(q.data_ptr(), sq.data_ptr(), k.data_ptr(),
+                                         sk.data_ptr(), v.data_ptr(), sv.data_ptr(),
+                                         out.data_ptr(), slices, n, d, cfg.blocks.Br,
+                                         cfg.blocks.Bc, flags,
+                                         au.data_ptr() if au is not None else None, sp))
+    _join(stream, qv.device, au)
     if au is not None:
         raw = au.cpu().numpy()
         w = raw[:2].view("int32")
@@ -238,6 +267,67 @@ def int_flash_attention(inputs: QuantizedAttentionInputs,
         audit.row_max_block_hits_127 = bool(w[2])
         audit.rows_audited = int(raw[2])
     return out
+
+
+def _check_shapes(inputs: QuantizedAttentionInputs) -> None:
+    """The cheap (no device sync) part of QuantizedAttentionInputs.validate
+    plus dtypes: what the kernels need to stay in bounds."""
+    qv = inputs.q.values
+    if qv.dim() < 2 or qv.shape[-2] < 1 or qv.shape[-1] < 1:
+        raise ValueError("quantized attention inputs: empty q")
+    for name, t in (("k", inputs.k.values), ("v", inputs.v.values)):
+        if tuple(t.shape) != tuple(qv.shape):
+            raise ValueError(f"quantized attention inputs: q, k, v must all be "
+                             f"{qv.shape[-2]}x{qv.shape[-1]} (got {name} {tuple(t.shape)})")
+    for name, sc, shape in (("q", inputs.q.scales, qv.shape[:-1]),
+                            ("k", inputs.k.scales, qv.shape[:-1]),
+                            ("v", inputs.v.scale, qv.shape[:-2])):
+        _require_cuda(sc, torch.float32, f"quantized attention inputs: {name} scales")
+        if tuple(sc.shape) != tuple(shape):
+            raise ValueError(f"quantized attention inputs: bad {name} scale shape "
+                             f"{tuple(sc.shape)}")
+        if sc.device != qv.device:
+            raise ValueError("quantized attention inputs: tensors on different devices")
+
+
+def int_flash_attention_dump(inputs: QuantizedAttentionInputs,
+                             cfg: Optional[AttentionConfig] = None, *,
+                             want_s: bool = True, want_p: bool = True,
+                             stream: Optional[torch.cuda.Stream] = None):
+    """Tolerance-mode forward that also returns what the tensor core computed:
+    ``(O, S, P)`` with S int32 ``[..., n, n]`` = Q.K^T read back from the
+    kind::i8 TMEM accumulator (the reference's int_gemm_nt,
+    attention.cpp:275-276 / gemm.cpp:32-46) and P uint8 ``[..., n, n]`` the
+    weight codes fed to P.V (attention.cpp:299-312); either may be None.
+    Needs Bc = 128 (the kernel's KV tile) or Bc >= n <= 128.  With ``causal``
+    only KV tiles at or below the diagonal are written (others stay 0)."""
+    cfg = cfg or AttentionConfig()
+    qv = inputs.q.values
+    for name, t in (("q", qv), ("k", inputs.k.values), ("v", inputs.v.values)):
+        _require_cuda(t, torch.int8, f"int_flash_attention: {name}")
+    inputs.validate()
+    cfg.validate()
+    n, d = qv.shape[-2], qv.shape[-1]
+    slices = qv.numel() // (n * d)
+    lead = tuple(qv.shape[:-2])
+    out = torch.empty(qv.shape, dtype=torch.float32, device=qv.device)
+    s_out = torch.zeros(lead + (n, n), dtype=torch.int32, device=qv.device) if want_s else None
+    p_out = torch.zeros(lead + (n, n), dtype=torch.uint8, device=qv.device) if want_p else None
+    flags = _lib.FLAG_FAST | _lib.FLAG_DUMP_S | \
+        (_lib.FLAG_SQRT_D if cfg.apply_sqrt_d_scaling else 0) | \
+        (_lib.FLAG_CAUSAL if cfg.causal else 0)
+    lib = _lib.load()
+    with torch.cuda.device(qv.device):
+        _lib.check(lib.ifa_int_flash_fwd_dump(
+            inputs.q.values.contiguous().data_ptr(), inputs.q.scales.contiguous().data_ptr(),
+            inputs.k.values.contiguous().data_ptr(), inputs.k.scales.contiguous().data_ptr(),
+            inputs.v.values.contiguous().data_ptr(),
+            inputs.v.scale.contiguous().reshape(-1).data_ptr(), out.data_ptr(), slices, n, d,
+            cfg.blocks.Br, cfg.blocks.Bc, flags,
+            s_out.data_ptr() if s_out is not None else None,
+            p_out.data_ptr() if p_out is not None else None, _stream_ptr(stream, qv.device)))
+    _join(stream, qv.device)
+    return out, s_out, p_out
 
 
 def half_int8_attention(q: QuantizedRows, k: QuantizedRows, v: torch.Tensor,
@@ -281,13 +371,18 @@ def half_int8_attention(q: QuantizedRows, k: QuantizedRows, v: torch.Tensor,
     vh = torch.empty(v.shape, dtype=torch.float16, device=v.device)
     if out is None:
         out = torch.empty(qv.shape, dtype=torch.float32, device=qv.device)
+    else:
+        _check_out(out, qv, "half_int8_attention")
     lib = _lib.load()
-    sp = _stream_ptr(stream)
-    _lib.check(lib.ifa_convert_f16(vc.data_ptr(), vc.numel(), vh.data_ptr(), sp))
-    _lib.check(lib.ifa_half_int8_fwd(qc.data_ptr(), sq.data_ptr(), kc.data_ptr(), sk.data_ptr(),
-                                     vh.data_ptr(), out.data_ptr(), slices, n, d,
-                                     cfg.blocks.Br, cfg.blocks.Bc,
-                                     _lib.FLAG_SQRT_D if cfg.apply_sqrt_d_scaling else 0, sp))
+    with torch.cuda.device(qv.device):
+        sp = _stream_ptr(stream, qv.device)
+        _lib.check(lib.ifa_convert_f16(vc.data_ptr(), vc.numel(), vh.data_ptr(), sp))
+        _lib.check(lib.ifa_half_int8_fwd(qc.data_ptr(), sq.data_ptr(), kc.data_ptr(),
+                                         sk.data_ptr(), vh.data_ptr(), out.data_ptr(), slices,
+                                         n, d, cfg.blocks.Br, cfg.blocks.Bc,
+                                         _lib.FLAG_SQRT_D if cfg.apply_sqrt_d_scaling else 0,
+                                         sp))
+    _join(stream, qv.device, vh)
     return out
 
 
@@ -317,11 +412,13 @@ def fp8_quantize_per_tensor(x: torch.Tensor, *, check_finite: bool = True,
     bad = torch.full((1,), _INT64_MAX, dtype=torch.int64, device=x.device) if check_finite \
         else None
     lib = _lib.load()
-    _lib.check(lib.ifa_fp8_quantize_per_tensor(x.data_ptr(), slices, rows, cols,
-                                               codes.data_ptr(), dec.data_ptr(), scale.data_ptr(),
-                                               ws.data_ptr(),
-                                               bad.data_ptr() if bad is not None else None,
-                                               _stream_ptr(stream)))
+    with torch.cuda.device(x.device):
+        _lib.check(lib.ifa_fp8_quantize_per_tensor(x.data_ptr(), slices, rows, cols,
+                                                   codes.data_ptr(), dec.data_ptr(),
+                                                   scale.data_ptr(), ws.data_ptr(),
+                                                   bad.data_ptr() if bad is not None else None,
+                                                   _stream_ptr(stream, x.device)))
+    _join(stream, x.device, bad, ws)
     if bad is not None and int(bad.item()) != _INT64_MAX:
         raise ValueError("fp8_e4m3_roundtrip: non-finite input")  # fp8.cpp:82-84
     return Fp8Tensor(codes, scale, dec)
@@ -351,14 +448,19 @@ def fp8_emulated_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
     q8, k8, v8 = (fp8_quantize_per_tensor(t, stream=stream) for t in (q, k, v))
     if out is None:
         out = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+    else:
+        _check_out(out, q, "fp8_emulated_attention")
     lib = _lib.load()
-    _lib.check(lib.ifa_fp8_attention_fwd(q8.codes.data_ptr(), q8.scale.data_ptr(),
-                                         k8.codes.data_ptr(), k8.scale.data_ptr(),
-                                         v8.decoded.data_ptr(), v8.scale.data_ptr(),
-                                         out.data_ptr(), slices, n, d, cfg.blocks.Br,
-                                         cfg.blocks.Bc,
-                                         _lib.FLAG_SQRT_D if cfg.apply_sqrt_d_scaling else 0,
-                                         _stream_ptr(stream)))
+    with torch.cuda.device(q.device):
+        _lib.check(lib.ifa_fp8_attention_fwd(q8.codes.data_ptr(), q8.scale.data_ptr(),
+                                             k8.codes.data_ptr(), k8.scale.data_ptr(),
+                                             v8.decoded.data_ptr(), v8.scale.data_ptr(),
+                                             out.data_ptr(), slices, n, d, cfg.blocks.Br,
+                                             cfg.blocks.Bc,
+                                             _lib.FLAG_SQRT_D if cfg.apply_sqrt_d_scaling
+                                             else 0, _stream_ptr(stream, q.device)))
+    _join(stream, q.device, q8.codes, q8.scale, q8.decoded, k8.codes, k8.scale, k8.decoded,
+          v8.codes, v8.scale, v8.decoded)
     return out
 
 

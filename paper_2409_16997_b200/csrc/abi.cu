@@ -50,6 +50,20 @@ __global__ void audit_init_kernel(ifa_pcode_audit* a) {
 
 namespace ifa_b200 {
 
+int current_device_sms() {
+    static std::atomic<int> sms_of[kMaxDevices] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    int sms = dev >= 0 && dev < kMaxDevices ? sms_of[dev].load(std::memory_order_relaxed) : 0;
+    if (sms <= 0) {
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+            sms <= 0)
+            sms = 148;
+        if (dev >= 0 && dev < kMaxDevices) sms_of[dev].store(sms, std::memory_order_relaxed);
+    }
+    return sms;
+}
+
 int set_error(int code, const std::string& msg) {
     g_err = msg;
     return code;
@@ -135,21 +149,15 @@ int ifa_quantize_per_tensor(const float* x, int64_t slices, int64_t rows, int64_
     return e == cudaSuccess ? IFA_OK : cuda_fail(e, "quantize_per_tensor");
 }
 
-int ifa_int_flash_fwd(const int8_t* q, const float* sq, const int8_t* k, const float* sk,
-                      const int8_t* v, const float* sv, float* o, int64_t slices, int64_t n,
-                      int64_t d, int64_t br, int64_t bc, uint32_t flags,
-                      ifa_pcode_audit* audit, void* stream) {
-    g_err.clear();
-    const int rc = ifa_b200::validate_fwd(slices, n, d, br, bc, flags);
-    if (rc != IFA_OK) return rc;
-    if (slices == 0) return IFA_OK;
-    if (((n + 127) / 128) * slices > INT32_MAX)
-        return fail(IFA_ENOTSUP, "int_flash_attention: more than 2^31 (q tile, slice) work items");
-    if (!q || !sq || !k || !sk || !v || !sv || !o)
-        return fail(IFA_EINVAL, "int_flash_attention: null pointer");
+namespace {
 
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    ifa_b200::AttnArgs a{q, sq, k, sk, v, sv, o, audit, slices, n, d, d, bc, flags};
+// ifa_int_flash_fwd and ifa_int_flash_fwd_dump after validation: stages
+// 16-byte-pitch copies of the codes when TMA needs them, then dispatches.
+int fwd_impl(const int8_t* q, const float* sq, const int8_t* k, const float* sk, const int8_t* v,
+             const float* sv, float* o, int64_t slices, int64_t n, int64_t d, int64_t bc,
+             uint32_t flags, ifa_pcode_audit* audit, const ifa_b200::AttnDump* dump,
+             cudaStream_t st) {
+    ifa_b200::AttnArgs a{q, sq, k, sk, v, sv, o, audit, slices, n, d, d, bc, flags, dump};
     const bool aligned = (reinterpret_cast<uintptr_t>(q) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(k) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(v) % 16 == 0);
@@ -171,12 +179,56 @@ int ifa_int_flash_fwd(const int8_t* q, const float* sq, const int8_t* k, const f
         a.v = padded + 2 * per;
         a.pitch = pitch;
     }
-    cudaError_t e = ifa_b200::launch_int_flash_fwd(a, st);
+    cudaError_t e = dump ? ifa_b200::launch_int_flash_pp(a, nullptr, st)
+                         : ifa_b200::launch_int_flash_fwd(a, st);
     if (padded) {
         const cudaError_t e2 = cudaFreeAsync(padded, st);
         if (e == cudaSuccess) e = e2;
     }
     return e == cudaSuccess ? IFA_OK : cuda_fail(e, "int_flash_attention");
+}
+
+}  // namespace
+
+int ifa_int_flash_fwd(const int8_t* q, const float* sq, const int8_t* k, const float* sk,
+                      const int8_t* v, const float* sv, float* o, int64_t slices, int64_t n,
+                      int64_t d, int64_t br, int64_t bc, uint32_t flags,
+                      ifa_pcode_audit* audit, void* stream) {
+    g_err.clear();
+    const int rc = ifa_b200::validate_fwd(slices, n, d, br, bc, flags);
+    if (rc != IFA_OK) return rc;
+    if (slices == 0) return IFA_OK;
+    if (((n + 127) / 128) * slices > INT32_MAX)
+        return fail(IFA_ENOTSUP, "int_flash_attention: more than 2^31 (q tile, slice) work items");
+    if (!q || !sq || !k || !sk || !v || !sv || !o)
+        return fail(IFA_EINVAL, "int_flash_attention: null pointer");
+    return fwd_impl(q, sq, k, sk, v, sv, o, slices, n, d, bc, flags, audit, nullptr,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int ifa_int_flash_fwd_dump(const int8_t* q, const float* sq, const int8_t* k, const float* sk,
+                           const int8_t* v, const float* sv, float* o, int64_t slices, int64_t n,
+                           int64_t d, int64_t br, int64_t bc, uint32_t flags, int32_t* s_out,
+                           uint8_t* p_codes, void* stream) {
+    g_err.clear();
+    flags &= ~IFA_FLAG_DUMP_S;  // implied by this entry point
+    const int rc = ifa_b200::validate_fwd(slices, n, d, br, bc, flags);
+    if (rc != IFA_OK) return rc;
+    if (slices == 0) return IFA_OK;
+    if (!(flags & IFA_FLAG_FAST))
+        return fail(IFA_EINVAL, "int_flash_attention dump: needs IFA_FLAG_FAST");
+    if (!(bc == 128 || (bc >= n && n <= 128)))
+        return fail(IFA_ENOTSUP, "int_flash_attention dump: the tolerance kernel's KV block is "
+                                 "128 keys (Bc = 128, or Bc >= n <= 128)");
+    if (n > 65536 || slices * n * n > (int64_t{1} << 40))
+        return fail(IFA_ENOTSUP, "int_flash_attention dump: slice too large for an n x n dump");
+    if (((n + 127) / 128) * slices > INT32_MAX)
+        return fail(IFA_ENOTSUP, "int_flash_attention: more than 2^31 (q tile, slice) work items");
+    if (!q || !sq || !k || !sk || !v || !sv || !o || (!s_out && !p_codes))
+        return fail(IFA_EINVAL, "int_flash_attention: null pointer");
+    const ifa_b200::AttnDump dump{s_out, p_codes};
+    return fwd_impl(q, sq, k, sk, v, sv, o, slices, n, d, bc, flags, nullptr, &dump,
+                    static_cast<cudaStream_t>(stream));
 }
 
 int ifa_quantize_per_tensor_v16(const float* x, int64_t slices, int64_t rows, int64_t cols,
@@ -208,6 +260,8 @@ int ifa_int_flash_fwd_v16(const int8_t* q, const float* sq, const int8_t* k, con
     const int rc = ifa_b200::validate_fwd(slices, n, d, br, bc, flags);
     if (rc != IFA_OK) return rc;
     if (slices == 0) return IFA_OK;
+    if (((n + 127) / 128) * slices > INT32_MAX)
+        return fail(IFA_ENOTSUP, "int_flash_attention: more than 2^31 (q tile, slice) work items");
     if (!q || !sq || !k || !sk || !v || !v_f16 || !sv || !o)
         return fail(IFA_EINVAL, "int_flash_attention: null pointer");
     ifa_b200::AttnArgs a{q, sq, k, sk, v, sv, o, nullptr, slices, n, d, d, bc, flags};

@@ -1260,23 +1260,11 @@ template <int D, bool GENERIC, bool FAST, bool QUAD = false>
 static cudaError_t launch_k(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                             const Params& p, int64_t slices, cudaStream_t stream) {
     const size_t smem = sizeof(Smem<D>) + 1024;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(int_flash_fwd_kernel<D, GENERIC, FAST, QUAD>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    const cudaError_t e = smem_attr_once<int_flash_fwd_kernel<D, GENERIC, FAST, QUAD>>(smem);
+    if (e != cudaSuccess) return e;
     // persistent: one CTA per SM (the kernel needs the whole SM: 512 TMEM
     // columns, ~170 KB of shared memory)
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
+    const int sms = current_device_sms();
     (void)slices;
     const int grid = p.items < sms ? p.items : sms;
     constexpr int threads = QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_THREADS;

@@ -570,21 +570,9 @@ static cudaError_t launch(const uint8_t* q, const float* sq, const uint8_t* k, c
     p.slices = static_cast<int32_t>(slices);
     p.items = p.q_tiles * p.slices;
     const size_t smem = sizeof(Smem<D>) + 1024;
-    static bool configured = false;
-    if (!configured) {
-        const cudaError_t e = cudaFuncSetAttribute(half_int8_fwd_kernel<D, FP8>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
+    const cudaError_t e = smem_attr_once<half_int8_fwd_kernel<D, FP8>>(smem);
+    if (e != cudaSuccess) return e;
+    const int sms = current_device_sms();
     const int grid = p.items < sms ? p.items : sms;
     half_int8_fwd_kernel<D, FP8><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
     return cudaGetLastError();

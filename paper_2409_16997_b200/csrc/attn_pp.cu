@@ -860,34 +860,14 @@ static cudaError_t run(const void* q, const void* k, const __half* v16, const Pa
         !make_map_v16(&tv, v16, p.slices, p.n_pad, D))
         return cudaErrorInvalidValue;
     const size_t smem = sizeof(Smem<D>) + 1024;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(int_flash_pp_kernel<D, false, MODE, false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e == cudaSuccess && MODE == kModeCodes) {
-            e = cudaFuncSetAttribute(int_flash_pp_kernel<D, true, MODE, false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem));
-            if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(int_flash_pp_kernel<D, false, MODE, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-            if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(int_flash_pp_kernel<D, true, MODE, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-        }
-        if (e != cudaSuccess) return e;
-        configured = true;
+    cudaError_t e = smem_attr_once<int_flash_pp_kernel<D, false, MODE, false>>(smem);
+    if (e == cudaSuccess && MODE == kModeCodes) {
+        e = smem_attr_once<int_flash_pp_kernel<D, true, MODE, false>>(smem);
+        if (e == cudaSuccess) e = smem_attr_once<int_flash_pp_kernel<D, false, MODE, true>>(smem);
+        if (e == cudaSuccess) e = smem_attr_once<int_flash_pp_kernel<D, true, MODE, true>>(smem);
     }
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
+    if (e != cudaSuccess) return e;
+    const int sms = current_device_sms();
     const int grid = p.items < sms ? p.items : sms;
     const bool ragged = p.n % BN != 0;
     if constexpr (MODE == kModeCodes) {
@@ -927,15 +907,17 @@ static Params make_params(const float* sq, const float* sk, const float* sv, flo
 
 template <int D>
 static cudaError_t launch(const AttnArgs& a, const uint16_t* v16_given, cudaStream_t stream) {
-    static bool pool_kept = false;
-    if (!pool_kept) {  // keep the per-call fp16 V workspace in the stream-ordered pool
+    static std::atomic<uint64_t> pool_kept{0};  // per device
+    {  // keep the per-call fp16 V workspace in the stream-ordered pool
         int dev = 0;
         cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        if (cudaGetDevice(&dev) == cudaSuccess && dev < kMaxDevices &&
+            !(pool_kept.load(std::memory_order_relaxed) & (uint64_t{1} << dev)) &&
+            cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
             uint64_t keep = UINT64_MAX;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            pool_kept.fetch_or(uint64_t{1} << dev, std::memory_order_relaxed);
         }
-        pool_kept = true;
     }
     __half* v16 = const_cast<__half*>(reinterpret_cast<const __half*>(v16_given));
     __half* owned = nullptr;

@@ -90,6 +90,18 @@ constexpr uint32_t kMagicS = IFA_WS_MAGIC_S;
 #ifndef IFA_WS_MUFU_LAG
 #define IFA_WS_MUFU_LAG 8
 #endif
+// softmax -> correction messages through named barriers (a warp blocked in
+// bar.sync takes no issue slots; the mbarrier wait of the correction warps
+// polls ~170 times per tile, ~870 issue slots) instead of mbarriers.
+// Measured: -18% instructions but 1.092 -> 1.130 ms at C2, so off.
+#ifndef IFA_WS_NAMED_MSG
+#define IFA_WS_NAMED_MSG 0
+#endif
+constexpr bool kNamedMsg = IFA_WS_NAMED_MSG != 0;
+// named barrier ids: 1, 2 group ping-pong; 3 + 2g + slot message full;
+// 7 + 2g + slot message empty (softmax warpgroup g + correction warpgroup)
+__host__ __device__ constexpr uint32_t msg_full_id(uint32_t g, uint32_t slot) { return 3 + 2 * g + slot; }
+__host__ __device__ constexpr uint32_t msg_empty_id(uint32_t g, uint32_t slot) { return 7 + 2 * g + slot; }
 #ifndef IFA_WS_CORR_SLEEP_NS
 #define IFA_WS_CORR_SLEEP_NS 0
 #endif
@@ -473,7 +485,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     // (a poll with a short sleep instead of the suspend-hint wait
                     // saves ~170 issue slots per tile of wake-ups but measured
                     // 3% slower: IFA_WS_CORR_SLEEP_NS)
-                    if (IFA_WS_CORR_SLEEP_NS > 0) {
+                    if (kNamedMsg) {
+                        named_bar_sync(msg_full_id(g, slot), 256);
+                    } else if (IFA_WS_CORR_SLEEP_NS > 0) {
                         const uint32_t bm = b_m_full + 16 * g + 8 * slot, par = (mcnt[g] >> 1) & 1;
                         while (!bar_try(bm, par)) __nanosleep(IFA_WS_CORR_SLEEP_NS);
                     } else {
@@ -481,8 +495,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                     const float a = sm.msg[g][slot][row];
                     if (warp == 8 && lane == 0) WS_TR(2, g, tcnt[g], 0);
-                    __syncwarp();
-                    if (lane == 0) bar_arrive(b_m_empty + 16 * g + 8 * slot);
+                    if (kNamedMsg) {
+                        named_bar_arrive(msg_empty_id(g, slot), 256);
+                    } else {
+                        __syncwarp();
+                        if (lane == 0) bar_arrive(b_m_empty + 16 * g + 8 * slot);
+                    }
                     ++mcnt[g];
                     const uint32_t t_o = t_row + 256 * g + 128;
                     if (j < jg) {
@@ -574,10 +592,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
         auto post = [&](float value) {  // one message to the correction warps
             const uint32_t slot = mc & 1;
-            if (mc >= 2) bar_wait(bm_empty + 8 * slot, ((mc >> 1) & 1) ^ 1u);
-            sm.msg[g][slot][row] = value;
-            __syncwarp();
-            if (lane == 0) bar_arrive(bm_full + 8 * slot);
+            if (kNamedMsg) {
+                if (mc >= 2) named_bar_sync(msg_empty_id(g, slot), 256);
+                sm.msg[g][slot][row] = value;
+                named_bar_arrive(msg_full_id(g, slot), 256);
+            } else {
+                if (mc >= 2) bar_wait(bm_empty + 8 * slot, ((mc >> 1) & 1) ^ 1u);
+                sm.msg[g][slot][row] = value;
+                __syncwarp();
+                if (lane == 0) bar_arrive(bm_full + 8 * slot);
+            }
             ++mc;
         };
 
@@ -697,9 +721,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         if (RAGGED && n - j * BN - 1 < kmax) kmax = n - j * BN - 1;
                         if (causal && j == diag && static_cast<int32_t>(row) < kmax)
                             kmax = static_cast<int32_t>(row);
+                        // finite: a zero Q row (sQ = 0) must not turn the masked
+                        // exponents into 0 * inf = NaN (the exp2 lag chain below
+                        // would carry it into the visible codes)
 #pragma unroll
                         for (int c = 0; c < 128; ++c)
-                            if (c > kmax) u[c] = -__int_as_float(0x7f800000);
+                            if (c > kmax) u[c] = -3.0e38f;
                     }
                     const float b = row_max128(u);
                     if (qw == 0 && lane == 0) WS_TR(0, g, tc, 6);
@@ -787,6 +814,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             post(l);  // item end: the correction warps write O * sV / l
         }
         if (pp && g == 0 && !first_turn) named_bar_sync(1, 256);  // group 1's last turn_end
+        if (kNamedMsg) {  // complete the correction warps' last releases of both slots
+            if (mc >= 2) named_bar_sync(msg_empty_id(g, mc & 1), 256);
+            if (mc >= 1) named_bar_sync(msg_empty_id(g, (mc + 1) & 1), 256);
+        }
     }
 
     tc_fence_before();
@@ -852,21 +883,13 @@ static bool make_map_v16(CUtensorMap* map, const __half* base, int64_t slices, i
            CUDA_SUCCESS;
 }
 
-constexpr int kMaxDevices = 64;
-
 template <int D, bool CAUSAL, bool RAGGED, bool DUMP>
 static cudaError_t launch_k(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                             const Params& p, int dev, int sms, cudaStream_t stream) {
     const size_t smem = sizeof(Smem<D>) + 1024;
-    // cudaFuncSetAttribute is per device: remember it per device
-    static bool configured[kMaxDevices] = {};
-    if (dev < 0 || dev >= kMaxDevices || !configured[dev]) {
-        const cudaError_t e = cudaFuncSetAttribute(int_flash_ws_kernel<D, CAUSAL, RAGGED, DUMP>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        if (dev >= 0 && dev < kMaxDevices) configured[dev] = true;
-    }
+    (void)dev;
+    const cudaError_t e = smem_attr_once<int_flash_ws_kernel<D, CAUSAL, RAGGED, DUMP>>(smem);
+    if (e != cudaSuccess) return e;
     const int grid = p.items < sms ? p.items : sms;
     int_flash_ws_kernel<D, CAUSAL, RAGGED, DUMP><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
     return cudaGetLastError();
@@ -880,16 +903,8 @@ static cudaError_t run(const int8_t* q, const int8_t* k, const __half* v16, cons
         !make_map_codes(&tk, k, p.slices, p.n, pitch, D) ||
         !make_map_v16(&tv, v16, p.slices, p.n_pad, D))
         return cudaErrorInvalidValue;
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    static int sms_of[kMaxDevices] = {};
-    int sms = dev < kMaxDevices ? sms_of[dev] : 0;
-    if (sms == 0) {
-        e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (e != cudaSuccess) return e;
-        if (dev < kMaxDevices) sms_of[dev] = sms;
-    }
+    const int dev = 0;
+    const int sms = current_device_sms();
     const bool ragged = p.n % BN != 0;
     if (p.s_dump != nullptr || p.p_dump != nullptr) {  // debug outputs: one generic instantiation
         if (causal) return launch_k<D, true, true, true>(tq, tk, tv, p, dev, sms, stream);

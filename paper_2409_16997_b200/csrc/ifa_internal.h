@@ -6,11 +6,32 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <string>
 
 #include "../../include/ifa_b200.h"
 
 namespace ifa_b200 {
+
+// ---- per-device launch state (a process may drive several GPUs) ----------
+constexpr int kMaxDevices = 64;
+// SM count of the current device, cached per device id (148 on a B200).
+int current_device_sms();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: apply it
+// once per (kernel, device).  Idempotent, so a race only repeats the call.
+template <auto Kernel>
+cudaError_t smem_attr_once(size_t smem) {
+    static std::atomic<uint64_t> done{0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = dev >= 0 && dev < kMaxDevices ? (uint64_t{1} << dev) : 0;
+    if (bit && (done.load(std::memory_order_relaxed) & bit)) return cudaSuccess;
+    e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+    if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_relaxed);
+    return e;
+}
 
 // Sets the thread-local ifa_last_error() message and returns `code`.
 int set_error(int code, const std::string& msg);

@@ -431,16 +431,7 @@ __global__ void __cluster_dims__(kSliceCluster, 1, 1) __launch_bounds__(512)
 }
 
 // ------------------------------------------------------------------ launchers
-static int sm_count() {
-    static int n = 0;
-    if (n == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
+static int sm_count() { return current_device_sms(); }
 
 cudaError_t launch_quantize_per_row(const float* x, int64_t rows, int64_t cols, int8_t* codes,
                                     float* scales, int64_t* bad, cudaStream_t stream) {

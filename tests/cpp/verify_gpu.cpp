@@ -130,6 +130,41 @@ int main() {
                     bad ? "FAIL" : "ok  ");
         failures += bad;
     }
+    // The tolerance kernel through the same plugin signature (IntFlashFn,
+    // verify.hpp:15-16) and the full-INT8 step from float matrices
+    // (eval.cpp:98-102): vs the reference library on the same inputs.
+    {
+        int bad = 0;
+        const int64_t shapes[][3] = {{1024, 64, 128}, {4096, 128, 128}, {384, 128, 128},
+                                     {300, 100, 128}, {96, 64, 300}};
+        for (int t = 0; t < 5; ++t) {
+            const int64_t n = shapes[t][0], d = shapes[t][1];
+            auto gen = [&](int role) {
+                return ifa::generate(t % 2 ? ifa::ActivationSpec::uniform(-0.5, 0.5, 501 + 3 * t + role)
+                                           : ifa::ActivationSpec::normal(0.0, 1.0, 501 + 3 * t + role),
+                                     n, d);
+            };
+            const ifa::FloatMatrix q = gen(0), k = gen(1), v = gen(2);
+            ifa::AttentionConfig cfg;
+            cfg.blocks = ifa::BlockSpec{64, shapes[t][2]};
+            const ifa::QuantizedAttentionInputs in{ifa::quantize_per_row(q), ifa::quantize_per_row(k),
+                                                   ifa::quantize_per_tensor(v)};
+            const ifa::FloatMatrix want = ifa::int_flash_attention(in, cfg);
+            const double e_fast = ifa::mre(want, ifa_gpu::int_flash_attention_fast(in, cfg));
+            const double e_full = ifa::mre(want, ifa_gpu::full_int8_attention(q, k, v, cfg, true));
+            const ifa::FloatMatrix exact = ifa_gpu::full_int8_attention(q, k, v, cfg, false);
+            const bool bitwise = same_bits(want.data(), exact.data(), n * d);
+            if (!(e_fast <= 1e-5) || !(e_full <= 1e-5) || !bitwise) {
+                std::printf("FAIL  n=%lld d=%lld fast MRE %.3g full-step MRE %.3g exact bitwise %d\n",
+                            static_cast<long long>(n), static_cast<long long>(d), e_fast, e_full,
+                            bitwise ? 1 : 0);
+                ++bad;
+            }
+        }
+        std::printf("%s int_flash_attention_fast / full_int8_attention drop-ins vs the reference\n",
+                    bad ? "FAIL" : "ok  ");
+        failures += bad;
+    }
     // Exceptions keep the reference's types and messages.
     {
         ifa::QuantizedAttentionInputs in;

@@ -69,6 +69,12 @@ class Oracle:
         L.ifa_or_int_flash_attention.argtypes = [
             _i8p, _f32p, _i8p, _f32p, _i8p, C.c_float, C.c_int64, C.c_int64, C.c_int64,
             C.c_int64, C.c_uint32, _f32p, C.POINTER(Audit)]
+        L.ifa_or_int_flash_attention_pcodes.argtypes = [
+            _i8p, _f32p, _i8p, _f32p, _i8p, C.c_float, C.c_int64, C.c_int64, C.c_int64,
+            C.c_int64, C.c_uint32, _f32p, C.c_void_p]
+        L.ifa_or_int_flash_attention_rows.argtypes = [
+            _i8p, _f32p, _i8p, _f32p, _i8p, C.c_float, C.c_int64, C.c_int64, C.c_int64,
+            C.c_int64, C.c_uint32, C.c_int64, C.c_int64, _f32p]
         L.ifa_or_int_flash_attention_batched.argtypes = [
             _i8p, _f32p, _i8p, _f32p, _i8p, _f32p, C.c_int64, C.c_int64, C.c_int64,
             C.c_int64, C.c_int64, C.c_uint32, _f32p, C.c_int]
@@ -155,6 +161,31 @@ class Oracle:
         if rc:
             raise ValueError("int_flash_attention: invalid argument")
         return (out, au.as_tuple()) if audit else out
+
+    def int_flash_pcodes(self, q, sq, k, sk, v, sv, br=128, bc=128, flags=0):
+        """(O, P codes [n][n] uint8) of int_flash_attention (attention.cpp:299-312)."""
+        q, k, v = _i8(q), _i8(k), _i8(v)
+        n, d = q.shape
+        out = np.empty((n, d), np.float32)
+        codes = np.zeros((n, n), np.uint8)
+        rc = self.lib.ifa_or_int_flash_attention_pcodes(
+            q, _f32(sq), k, _f32(sk), v, float(sv), n, d, br, bc, flags, out,
+            codes.ctypes.data_as(C.c_void_p))
+        if rc:
+            raise ValueError("int_flash_pcodes: invalid argument")
+        return out, codes
+
+    def int_flash_rows(self, q, sq, k, sk, v, sv, row_begin, row_end, br=128, bc=128,
+                       flags=0):
+        """Rows [row_begin, row_end) of int_flash_attention's O (row blocks are
+        independent, attention.cpp:267); the other rows of the result are NaN."""
+        q, k, v = _i8(q), _i8(k), _i8(v)
+        n, d = q.shape
+        out = np.full((n, d), np.nan, np.float32)
+        if self.lib.ifa_or_int_flash_attention_rows(q, _f32(sq), k, _f32(sk), v, float(sv), n,
+                                                    d, br, bc, flags, row_begin, row_end, out):
+            raise ValueError("int_flash_rows: invalid argument")
+        return out
 
     def int_flash_attention_batched(self, q, sq, k, sk, v, sv, br=128, bc=128, flags=0,
                                     threads=None):
