@@ -220,7 +220,8 @@ int ifa_full_int8_attention_host(const float* q, const float* k, const float* v,
 /* Host-buffer forms of the §8(f) variants (what include/ifa_b200.hpp's
  * ifa_gpu::half_int8_attention / fp8_emulated_attention call):
  *   ifa_half_int8_fwd_host: int8 Q/K codes + per-row scales and f32 V (host)
- *     -> f32 O (host); V is converted to fp16 on the device.
+ *     -> f32 O (host); V is converted to fp16 on the device.  |V| > 65504
+ *     (outside fp16) is rejected with IFA_EINVAL instead of producing inf. 
  *   ifa_fp8_emulated_attention_host: f32 Q, K, V (host) -> f32 O (host): the
  *     three e4m3 roundtrips and the FP8 forward; non-finite input returns
  *     IFA_EINVAL "fp8_e4m3_roundtrip: non-finite input" (fp8.cpp:82-84). */

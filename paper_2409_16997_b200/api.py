@@ -368,6 +368,11 @@ def half_int8_attention(q: QuantizedRows, k: QuantizedRows, v: torch.Tensor,
     qc, kc = qv.contiguous(), kv.contiguous()
     sq, sk = q.scales.contiguous(), k.scales.contiguous()
     vc = v.contiguous()
+    # the kernel feeds V to the tensor core as fp16: |V| beyond the fp16
+    # range (65504) would become inf, so refuse it instead of returning inf/NaN
+    if vc.numel() and float(vc.abs().max()) > 65504.0:
+        raise ValueError("half_int8_attention: |v| exceeds the fp16 range (65504) of the "
+                         "sm_100a kernel")
     vh = torch.empty(v.shape, dtype=torch.float16, device=v.device)
     if out is None:
         out = torch.empty(qv.shape, dtype=torch.float32, device=qv.device)

@@ -220,7 +220,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
                 const float* sk_slice = p.sk + static_cast<int64_t>(slice) * n;
                 // FP8: s = S / (sQ sK) for every key of the slice
-                const float c8 = FP8 ? __fdiv_rn(p.sk_mul, __fmul_rn(p.sq[slice], p.sk[slice])) : 0.0f;
+                // all-zero Q or K slice: scale 0, codes 0, scores 0 (fp8.cpp:78-97)
+                const float sqk = FP8 ? __fmul_rn(p.sq[slice], p.sk[slice]) : 0.0f;
+                const float c8 = FP8 && sqk != 0.0f ? __fdiv_rn(p.sk_mul, sqk) : 0.0f;
                 for (int32_t key0 = 0; key0 < n; key0 += BN) {
                     const uint32_t st = kv.idx;
                     if (i >= STAGES) bar_wait(b_kv_empty + 8 * st, kv.phase ^ 1u);
@@ -478,7 +480,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (row_ok && c_base < p.d) {
                 // FP8: V was restored as decode(code) / sV (fp8.cpp:94)
                 const float inv =
-                    FP8 ? __fdiv_rn(__fdiv_rn(1.0f, l), p.sv[slice]) : __fdiv_rn(1.0f, l);
+                    FP8 ? (p.sv[slice] == 0.0f ? 0.0f : __fdiv_rn(__fdiv_rn(1.0f, l), p.sv[slice]))
+                        : __fdiv_rn(1.0f, l);
                 float* orow = p.o + (static_cast<int64_t>(slice) * n + grow) * p.d + c_base;
                 if (p.d % 4 == 0 && c_base + NCOL <= p.d) {
 #pragma unroll

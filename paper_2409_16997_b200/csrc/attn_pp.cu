@@ -311,7 +311,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     if (i >= KST) bar_wait(b_k_empty + 8 * ks, kr.phase ^ 1u);
                     float4 k4;
                     if constexpr (MODE == kModeFp8) {  // s = S / (sQ sK): one constant per slice
-                        const float c8 = __fdiv_rn(p.sk_mul, __fmul_rn(p.sq[slice], p.sk[slice]));
+                        // an all-zero Q or K slice has scale 0 and zero codes: its
+                        // scores are 0 (fp8_e4m3_roundtrip returns zeros, fp8.cpp:78-97)
+                        const float sqk = __fmul_rn(p.sq[slice], p.sk[slice]);
+                        const float c8 = sqk == 0.0f ? 0.0f : __fdiv_rn(p.sk_mul, sqk);
                         k4 = make_float4(c8, c8, c8, c8);
                     } else {
                         const int32_t key = key0 + 4 * lane;
@@ -723,7 +726,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 else if constexpr (MODE == kModeHalf)
                     f[r] = __fdiv_rn(1.0f, lt);  // finalize_softmax_state (attention.cpp:139-149)
                 else
-                    f[r] = __fdiv_rn(__fdiv_rn(1.0f, lt), p.sv[slice]);  // V = decode / sV
+                    // V = decode / sV; an all-zero V slice (sV = 0) gives O = 0
+                    f[r] = p.sv[slice] == 0.0f ? 0.0f : __fdiv_rn(__fdiv_rn(1.0f, lt), p.sv[slice]);
             }
             bar_wait(bo_full, wi & 1);
             tc_fence_after();

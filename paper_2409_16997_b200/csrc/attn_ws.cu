@@ -73,14 +73,20 @@ constexpr float kLog2_127 = 6.9886846867721655f;
 #define IFA_WS_POLY_EVERY 0
 #endif
 constexpr int kPolyEvery = IFA_WS_POLY_EVERY;
-// S accumulates onto 0x4B400000 in TMEM (the softmax writes the constant
-// back after reading S): the int32 result's bits are the float 1.5 * 2^23 + S.
-// Measured slower (C2 1.09 -> 1.38 ms: the accumulate-mode S MMA and the
-// 64 KiB of constant stores per tile slow the TMEM loads), so off by default.
+// S accumulates onto 0x4B400000 in TMEM: the int32 result's bits are the
+// float 1.5 * 2^23 + S, so float(S) is one exact packed subtract (no integer
+// add per element).
+//   1: the softmax warps write the constant back after reading S (measured
+//      slower, C2 1.09 -> 1.38 ms: 64 KiB of tcgen05.st per tile on the math
+//      warps);
+//   2: the MMA-issuing thread refills the S columns with tcgen05.cp from a
+//      4 KiB constant block in shared memory right before the S MMAs (the
+//      tensor core's queue runs them in order; no math-warp work).
 #ifndef IFA_WS_MAGIC_S
 #define IFA_WS_MAGIC_S 0
 #endif
 constexpr uint32_t kMagicS = IFA_WS_MAGIC_S;
+constexpr uint32_t kMagicSoft = kMagicS == 1 ? 1u : 0u;  // softmax-side fill
 // float(S) by I2F (quarter-rate pipe of its own) instead of the integer
 // magic add + packed subtract
 #ifndef IFA_WS_I2F
@@ -132,6 +138,7 @@ struct alignas(1024) Smem {
     uint8_t p[2][BM * BN * 2];   // [group] fp16 P, K-major SW128: 2 atoms of 64 keys
     float sk[KST][BN];           // K scales * log2(e) [/ sqrt(d)] of the stage
     float msg[2][2][BM];         // [group][slot][row]: alpha of a tile, l at the item end
+    uint32_t magic[kMagicS == 2 ? 1024 : 4];  // tcgen05.cp source: 128 rows x 32 B of 0x4B400000
     uint64_t q_full, q_empty;
     uint64_t k_full[KST], k_empty[KST], v_full[VST], v_empty[VST];
     uint64_t s_full[2], s_empty[2], p_full[2], p_empty[2], o_ready[2];
@@ -309,6 +316,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         fence_barrier_init();
     }
     if (warp == kWarpMma) tmem_alloc<TMEM_COLS>(&sm.tmem_base);
+    if (kMagicS == 2) {
+        for (uint32_t i = threadIdx.x; i < 1024; i += NUM_THREADS) sm.magic[i] = 0x4B400000u;
+        fence_proxy_async_shared();  // read by the tensor core (tcgen05.cp)
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -391,6 +402,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     tc_fence_after();
                     const uint32_t q_base = smem_u32(sm.q[g]);
                     const uint32_t k_base = smem_u32(sm.k[ks]);
+                    if (kMagicS == 2) {
+                        // no-swizzle K-major 128 x 32 B: 8-row x 16 B core
+                        // matrices, LBO 128 B (K), SBO 256 B (8-row groups)
+                        const uint64_t cdesc = smem_desc(smem_u32(sm.magic), 128, 256, 0);
+#pragma unroll
+                        for (int c = 0; c < BN / 8; ++c) tmem_cp_128x256b(d_s + 8 * c, cdesc);
+                    }
 #pragma unroll
                     for (int kk = 0; kk < D / 32; ++kk) {
                         const uint64_t adesc = smem_desc(q_base + kk * 32, 16, kSbo, kLayout);
@@ -401,7 +419,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 };
                 if (blockIdx.x < p.items) {
                     bar_wait(b_q_full, 0);
-                    if (kMagicS) bar_wait(b_s_empty + 8 * g, 0);  // S filled with the constant
+                    if (kMagicSoft) bar_wait(b_s_empty + 8 * g, 0);  // S filled with the constant
                     issue_s(0, 0);
                 }
                 const uint32_t p_base = smem_u32(sm.p[g]);
@@ -429,7 +447,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             Ring<KST> nk = kr;
                             const int32_t ahead = last ? w.jt - j : 1;
                             for (int32_t a = 0; a < ahead; ++a) nk.advance();
-                            bar_wait(b_s_empty + 8 * g, (t + kMagicS) & 1);
+                            bar_wait(b_s_empty + 8 * g, (t + kMagicSoft) & 1);
                             issue_s(nk.idx, nk.phase);
                             WS_TR(1, g, t, 0);
                         }
@@ -607,7 +625,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
         // group 1 starts later, so the two groups' MUFU-heavy code phases
         // interleave instead of running in lockstep
-        if (kMagicS) {  // the first S of the kernel accumulates onto the constant
+        if (kMagicSoft) {  // the first S of the kernel accumulates onto the constant
 #pragma unroll
             for (int c = 0; c < 4; ++c) tmem_fill32(t_s + 32 * c, 0x4B400000u);
             tmem_wait_st();
@@ -668,7 +686,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         tmem_ld32(t_s + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&s[32 * c]));
                     tmem_wait_ld();
                     if (qw == 0 && lane == 0) WS_TR(0, g, tc, 4);
-                    if (kMagicS) {  // S(j+1) accumulates onto the constant again
+                    if (kMagicSoft) {  // S(j+1) accumulates onto the constant again
 #pragma unroll
                         for (int c = 0; c < 4; ++c) tmem_fill32(t_s + 32 * c, 0x4B400000u);
                         tmem_wait_st();

@@ -570,6 +570,14 @@ int ifa_half_int8_fwd_host(const int8_t* q, const float* sq, const int8_t* k, co
     if (slices == 0) return IFA_OK;
     if (!q || !sq || !k || !sk || !v || !o)
         return ifa_b200::set_error(IFA_EINVAL, "half_int8_attention: null pointer");
+    {  // V goes to the tensor core as fp16 (include/ifa_b200.h)
+        const size_t count = static_cast<size_t>(slices) * n * d;
+        for (size_t i = 0; i < count; ++i)
+            if (std::fabs(v[i]) > 65504.0f)
+                return ifa_b200::set_error(
+                    IFA_EINVAL, "half_int8_attention: |v| exceeds the fp16 range (65504) of the "
+                                "sm_100a kernel");
+    }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const size_t elems = static_cast<size_t>(slices) * n * d;
     const size_t rows = static_cast<size_t>(slices) * n;

@@ -326,6 +326,13 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
     d |= static_cast<uint64_t>(layout & 7) << 61;
     return d;
 }
+// tcgen05.cp of a 128-lane x 256-bit (8 columns of 32 bit) block from shared
+// memory into TMEM; issued by one thread, ordered with that thread's later
+// tcgen05.mma (both run in issue order on the tensor core's queue).
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc)
+                 : "memory");
+}
 // Instruction descriptor for kind::i8: D=S32, A=B=signed int8, dense.
 __host__ __device__ constexpr uint32_t idesc_i8(uint32_t m, uint32_t n, bool a_mn_major,
                                                 bool b_mn_major) {

@@ -103,3 +103,22 @@ def test_fp8_attention_batched(ifa, oracle):
         for hi in range(h):
             want = oracle.fp8_attention(x[0][bi, hi], x[1][bi, hi], x[2][bi, hi], 64, 64)
             _check(oracle, got[bi, hi], want, x[2][bi, hi])
+
+
+@pytest.mark.parametrize("zero", ["q", "k", "v", "qkv"])
+@pytest.mark.parametrize("n", [256, 200])
+def test_fp8_attention_zero_slices(ifa, oracle, zero, n):
+    """An all-zero Q, K or V slice has e4m3 scale 0: the reference's
+    roundtrip returns zeros there (fp8.cpp:78-97), so the scores are 0 (uniform
+    weights, O = mean of the restored V) or O = 0 -- never NaN."""
+    d = 64
+    q, k, v = oracle.slice_inputs("normal", n, d, seed=9)
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        if name in zero:
+            t[:] = 0.0
+    got = ifa.fp8_emulated_attention(_dev(q), _dev(k), _dev(v)).cpu().numpy()
+    want = oracle.fp8_attention(q, k, v, 64, 64)
+    assert np.isfinite(got).all()
+    assert np.isfinite(want).all()
+    scale = max(float(np.abs(want).max()), 1e-30)
+    assert float(np.abs(got - want).max()) <= 4e-3 * max(scale, float(np.abs(v).max())), zero

@@ -119,3 +119,17 @@ def test_half_int8_argument_errors(ifa):
         ifa.half_int8_attention(q48, q48, torch.randn(64, 48, device="cuda"))
     with pytest.raises(NotImplementedError):
         ifa.half_int8_attention(qq, qq, x, ifa.AttentionConfig(causal=True))
+
+
+def test_half_int8_rejects_v_outside_fp16(ifa, oracle):
+    """V reaches the tensor core as fp16: values beyond 65504 are refused
+    (ValueError) rather than turned into inf/NaN output."""
+    n, d = 128, 64
+    q, k, v = oracle.slice_inputs("normal", n, d, seed=4)
+    qc, qs = oracle.quantize_per_row(q)
+    kc, ks = oracle.quantize_per_row(k)
+    v[3, 5] = 1.0e6
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    with pytest.raises(ValueError, match="fp16 range"):
+        ifa.half_int8_attention(ifa.QuantizedRows(dev(qc), dev(qs)),
+                                ifa.QuantizedRows(dev(kc), dev(ks)), dev(v))

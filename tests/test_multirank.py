@@ -138,3 +138,10 @@ def test_bench_two_ranks_share_one_gpu(tmp_path):
     line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
     assert line["n_gpus"] == 2 and len(line["checksums"]) == 2
     assert line["config"]["slices_per_rank"] == 1024 and line["scaling"] == "strong"
+    # per-rank parity: sampled slices of BOTH ranks gathered to rank 0 and
+    # checked against the oracle; whole-job MRE vs fp64 from summed partials
+    par = line["parity_spot_check"]
+    assert sorted({p["rank"] for p in par["per_rank"]}) == [0, 1]
+    assert par["all_ok"], par
+    mre = line["mre_vs_fp64"]
+    assert mre["slices"] == 4 and 0.02 < mre["value"] < 0.045, mre

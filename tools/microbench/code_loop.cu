@@ -47,6 +47,34 @@ __global__ void __launch_bounds__(256, 1) bench(int iters, unsigned long long* c
     __syncthreads();
     const unsigned long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
+        if (MODE == 3) {  // attn_ws.cu order: all 128 exp2 first, then pack (lag 8 pairs)
+            float2 y[64];
+#pragma unroll
+            for (int k = 0; k < 64; ++k) {
+                const float2 t = ffma2(make_float2(u[2 * k], u[2 * k + 1]), make_float2(sq, sq),
+                                       make_float2(cr, cr));
+                y[k] = make_float2(ex2(t.x), ex2(t.y));
+            }
+#pragma unroll
+            for (int ch = 0; ch < 16; ++ch) {
+                uint32_t wd[4];
+                const int dep = 4 * ch + 3 + 8 < 63 ? 4 * ch + 3 + 8 : 63;
+                const float mg = __fmaf_rn(0.0f, y[dep].y, 12582912.0f);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 c = fadd2(y[4 * ch + e], make_float2(mg, mg));
+                    wd[e] = prmt(__float_as_uint(c.x), __float_as_uint(c.y), 0x5410u);
+                }
+                acc += wd[0] + wd[1];
+                acc += wd[2] + wd[3];
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(static_cast<uint32_t>(
+                                 __cvta_generic_to_shared(&p[warp][lane][4 * ((ch & 7) ^ (lane & 7))]))),
+                             "r"(wd[0]), "r"(wd[1]), "r"(wd[2]), "r"(wd[3])
+                             : "memory");
+            }
+            cr += 1e-7f;
+            continue;
+        }
 #pragma unroll
         for (int ch = 0; ch < 16; ++ch) {
             uint32_t wd[4];
@@ -103,5 +131,6 @@ int main() {
     for (int w : {4, 8}) run<0>(w);
     for (int w : {4, 8}) run<1>(w);
     for (int w : {4, 8}) run<2>(w);
+    for (int w : {4, 8}) run<3>(w);
     return 0;
 }
