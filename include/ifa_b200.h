@@ -55,7 +55,7 @@ extern "C" {
  * requantization, per-block float rescale) with one MUFU exp2 per code and no
  * exactness guard.  int8 codes, scales and int32 S are unaffected; O agrees
  * with the reference within the tolerance tests/test_gpu_parity.py states
- * (MRE <= 5e-5, max|dO| <= the reference's multi-block bound 2/127*max|V|*sV,
+ * (MRE <= 2e-5, max|dO| <= the reference's multi-block bound 2/127*max|V|*sV,
  * verify.cpp:65-70).  Ignored when an audit is requested. */
 #define IFA_FLAG_FAST 4u
 
@@ -142,6 +142,29 @@ int ifa_int_flash_fwd_v16(const int8_t* q, const float* sq, const int8_t* k, con
                           const int8_t* v, const uint16_t* v_f16, const float* sv, float* o,
                           int64_t slices, int64_t n, int64_t d, int64_t br, int64_t bc,
                           uint32_t flags, void* stream);
+
+/* ---- one whole step, quantization streamed into the attention -----------
+ * ifa_int8_attention_step: quantize_per_row(Q), quantize_per_row(K),
+ *   quantize_per_tensor(V) per slice (+ the fp16 V codes) and the tolerance
+ *   attention, from f32 DEVICE q, k, v [slices][n][d] into the caller's code
+ *   / scale buffers (same layouts as above) and o.  Results are exactly
+ *   those of the separate calls.  When the two-Q-tile kernel applies
+ *   (IFA_FLAG_FAST, non-causal, Bc = 128, n % 128 == 0, d in {64, 128}) the
+ *   first slices (enough for the attention's first wave) are quantized on the
+ *   whole GPU, then the quantizer runs on a few SMs (IFA_B200_QUANT_SMS,
+ *   default 12) concurrently with the attention kernel on the rest, one
+ *   whole slice per CTA: the attention waits per slice on a ready word in
+ *   sync_ws instead of on the whole quantization.  Otherwise the calls run
+ *   one after the other on `stream`.
+ *   sync_ws: DEVICE uint32[2 * slices], zeroed before the first call and
+ *   then owned by this sequence of calls; epoch: 1 on the first call, +1 on
+ *   every later call with the same sync_ws.  nonfinite_index as for the
+ *   quantizers (smallest flat index of a NaN/Inf in any of q, k, v). */
+int ifa_int8_attention_step(const float* q, const float* k, const float* v, int8_t* qc,
+                            float* sq, int8_t* kc, float* sk, int8_t* vc, float* sv,
+                            uint16_t* v16, float* o, int64_t* nonfinite_index,
+                            uint32_t* sync_ws, uint32_t epoch, int64_t slices, int64_t n,
+                            int64_t d, int64_t br, int64_t bc, uint32_t flags, void* stream);
 
 /* ---- half-INT8 attention ----------------------------
  * ifa_half_int8_fwd  replaces ifa::half_int8_attention (attention.hpp:93-96,

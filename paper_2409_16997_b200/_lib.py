@@ -30,6 +30,7 @@ EXPORTED_SYMBOLS = (
     "ifa_quantize_per_tensor",
     "ifa_int_flash_fwd",
     "ifa_int_flash_fwd_dump",
+    "ifa_int8_attention_step",
     "ifa_half_int8_fwd",
     "ifa_convert_f16",
     "ifa_quantize_per_tensor_v16",
@@ -95,6 +96,9 @@ def load() -> C.CDLL:
     lib.ifa_int_flash_fwd_dump.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i64,
                                            i64, u32, vp, vp, vp]
     lib.ifa_int_flash_fwd_dump.restype = C.c_int
+    lib.ifa_int8_attention_step.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                            u32, i64, i64, i64, i64, i64, u32, vp]
+    lib.ifa_int8_attention_step.restype = C.c_int
     lib.ifa_half_int8_fwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, u32, vp]
     lib.ifa_half_int8_fwd.restype = C.c_int
     lib.ifa_convert_f16.argtypes = [vp, i64, vp, vp]

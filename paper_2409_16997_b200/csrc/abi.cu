@@ -10,6 +10,8 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <mutex>
 #include <string>
 
 #include "code_bounds.h"
@@ -274,6 +276,105 @@ int ifa_int_flash_fwd_v16(const int8_t* q, const float* sq, const int8_t* k, con
     }
     return ifa_int_flash_fwd(q, sq, k, sk, v, sv, o, slices, n, d, br, bc, flags, nullptr,
                              stream);
+}
+
+namespace {
+// Per-device side stream + fork/join events of the streamed step.
+struct StepStreams {
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+cudaError_t step_streams(StepStreams** out) {
+    static StepStreams per_dev[ifa_b200::kMaxDevices];
+    static std::mutex mu;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= ifa_b200::kMaxDevices) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lock(mu);
+    StepStreams& s = per_dev[dev];
+    if (!s.side) {
+        if ((e = cudaStreamCreateWithFlags(&s.side, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming)) != cudaSuccess)
+            return e;
+    }
+    *out = &s;
+    return cudaSuccess;
+}
+}  // namespace
+
+int ifa_int8_attention_step(const float* q, const float* k, const float* v, int8_t* qc,
+                            float* sq, int8_t* kc, float* sk, int8_t* vc, float* sv,
+                            uint16_t* v16, float* o, int64_t* nonfinite_index,
+                            uint32_t* sync_ws, uint32_t epoch, int64_t slices, int64_t n,
+                            int64_t d, int64_t br, int64_t bc, uint32_t flags, void* stream) {
+    g_err.clear();
+    const int rc = ifa_b200::validate_fwd(slices, n, d, br, bc, flags);
+    if (rc != IFA_OK) return rc;
+    if (slices == 0) return IFA_OK;
+    if (!q || !k || !v || !qc || !sq || !kc || !sk || !vc || !sv || !v16 || !o || !sync_ws)
+        return fail(IFA_EINVAL, "int8_attention_step: null pointer");
+    if (epoch == 0) return fail(IFA_EINVAL, "int8_attention_step: epoch starts at 1");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int sms = ifa_b200::current_device_sms();
+    int qctas = 12;
+    if (const char* env = std::getenv("IFA_B200_QUANT_SMS")) qctas = std::atoi(env);
+    const int64_t bce = bc < n ? bc : n;
+    const bool streamed = (flags & IFA_FLAG_FAST) && !(flags & IFA_FLAG_CAUSAL) &&
+                          (bce == 128 || (bce == n && n <= 128)) && n % 128 == 0 &&
+                          (d == 64 || d == 128) && qctas >= 1 && qctas <= sms / 4 &&
+                          !ifa_b200::int_flash_ws_enabled() && slices <= INT32_MAX / 64;
+    if (!streamed) {  // same results, quantize then attention on `stream`
+        uint32_t* ws = sync_ws + slices;  // the per-tensor quantizer's scratch
+        int r = ifa_quantize_per_row(q, slices * n, d, qc, sq, nonfinite_index, stream);
+        if (r == IFA_OK) r = ifa_quantize_per_row(k, slices * n, d, kc, sk, nonfinite_index, stream);
+        if (r == IFA_OK)
+            r = ifa_quantize_per_tensor_v16(v, slices, n, d, vc, v16, sv, ws, nonfinite_index,
+                                            stream);
+        if (r != IFA_OK) return r;
+        return ifa_int_flash_fwd_v16(qc, sq, kc, sk, vc, v16, sv, o, slices, n, d, br, bc, flags,
+                                     stream);
+    }
+    StepStreams* ss = nullptr;
+    cudaError_t e = step_streams(&ss);
+    if (e != cudaSuccess) return cuda_fail(e, "int8_attention_step: streams");
+    uint32_t* ready = sync_ws;
+    const int actas = sms - qctas;
+    // The first slices are quantized on the whole GPU before the attention
+    // starts (its first wave needs ~actas / pairs slices at once); the
+    // streamed quantizer takes the rest, ahead of the attention.
+    const int64_t pairs = (n + 255) / 256;
+    int64_t s0 = (2 * actas + pairs - 1) / pairs;
+    if (s0 < 8) s0 = 8;
+    if (s0 > slices) s0 = slices;
+    // host order: the streamed quantizer first (it then owns its SMs, and
+    // under a serialising profiler it completes before anything waits on it)
+    if ((e = cudaEventRecord(ss->fork, st)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(ss->side, ss->fork, 0)) != cudaSuccess)
+        return cuda_fail(e, "int8_attention_step: fork");
+    e = ifa_b200::launch_stream_quantize(q, k, v, s0, slices, n, d, qc, sq, kc, sk, vc, sv, v16,
+                                         nonfinite_index, ready, epoch, qctas, ss->side);
+    if (e != cudaSuccess) return cuda_fail(e, "int8_attention_step: quantize");
+    {  // slices [0, s0) on `stream`, full GPU
+        uint32_t* ws = sync_ws + slices;  // per-tensor quantizer scratch
+        int r = ifa_quantize_per_row(q, s0 * n, d, qc, sq, nonfinite_index, stream);
+        if (r == IFA_OK) r = ifa_quantize_per_row(k, s0 * n, d, kc, sk, nonfinite_index, stream);
+        if (r == IFA_OK)
+            r = ifa_quantize_per_tensor_v16(v, s0, n, d, vc, v16, sv, ws, nonfinite_index, stream);
+        if (r != IFA_OK) return r;
+    }
+    ifa_b200::AttnArgs a{qc, sq, kc, sk, vc, sv, o, nullptr, slices, n, d, d, bc, flags};
+    a.ready = ready;
+    a.ready_target = epoch;
+    a.ready_from = static_cast<int32_t>(s0);
+    a.max_ctas = actas;
+    e = ifa_b200::launch_int_flash_pp(a, v16, st);
+    if (e != cudaSuccess) return cuda_fail(e, "int8_attention_step: attention");
+    if ((e = cudaEventRecord(ss->join, ss->side)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(st, ss->join, 0)) != cudaSuccess)
+        return cuda_fail(e, "int8_attention_step: join");
+    return IFA_OK;
 }
 
 int ifa_half_int8_fwd(const int8_t* q, const float* sq, const int8_t* k, const float* sk,

@@ -106,7 +106,36 @@ struct Params {
     float sk_mul;  // log2(e) [* 1/sqrt(d)]: scores are kept in the log2 domain
     uint32_t flags;
     int32_t pairs, slices, items;
+    // streamed step (ifa_int8_attention_step): the inputs of slice s are
+    // ready once ready[s] >= ready_target (written by the concurrently
+    // running stream quantizer, quant.cu); null = inputs already complete
+    const uint32_t* ready;
+    uint32_t ready_target;
+    int32_t ready_from;  // slices below it were quantized before the launch
+    int32_t max_ctas;    // grid cap (SMs left to the quantizer), 0 = all SMs
 };
+
+// Waits until the quantizer has published slice `slice` (acquire), then
+// orders this thread's later async-proxy (TMA) reads after it.  Traps after
+// ~4 s instead of hanging (a quantizer that cannot make progress).
+__device__ __forceinline__ void wait_slice_ready(const Params& p, int32_t slice) {
+    if (p.ready == nullptr || slice < p.ready_from) return;
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.ready + slice) : "memory");
+    if (v < p.ready_target) {
+        uint64_t t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        do {
+            __nanosleep(256);
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.ready + slice)
+                         : "memory");
+            uint64_t t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 4000000000ull) __trap();
+        } while (v < p.ready_target);
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 
 template <int N>
 struct Ring {
@@ -225,7 +254,9 @@ __device__ __forceinline__ void mma_f8_ss(uint32_t d_tmem, uint64_t a_desc, uint
 
 // RAGGED: n is not a multiple of 128 (the last KV tile masks missing keys);
 // a template parameter so the common case carries no masking code.
-template <int D, bool CAUSAL, int MODE, bool RAGGED>
+// STREAMED: the inputs of a slice are waited for per item (streamed step); a
+// separate instantiation because the check costs the math warps registers.
+template <int D, bool CAUSAL, int MODE, bool RAGGED, bool STREAMED = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     int_flash_pp_kernel(const __grid_constant__ CUtensorMap tm_q,
                         const __grid_constant__ CUtensorMap tm_k,
@@ -299,6 +330,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x, ++wi) {
                 const PWork w = pwork(idx, p, causal, J);
                 const int32_t q0 = w.pair * 2 * BM, slice = w.slice;
+                if constexpr (STREAMED) wait_slice_ready(p, slice);  // every lane: sK loads below
                 if (lane == 0) {
                     if (wi >= 1) bar_wait(b_q_empty, (wi - 1) & 1);
                     mbar_arrive_expect_tx(&sm.q_full, 2 * BM * D);
@@ -478,6 +510,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int32_t diag = causal ? 2 * w.pair + static_cast<int32_t>(g) : -1;
             const int32_t q0 = w.pair * 2 * BM + static_cast<int32_t>(g) * BM;
             const int32_t slice = w.slice;
+            if constexpr (STREAMED) wait_slice_ready(p, slice);  // sQ, sV of a streamed step
             int32_t grow[2];
             float sq[2];
 #pragma unroll
@@ -872,10 +905,17 @@ static cudaError_t run(const void* q, const void* k, const __half* v16, const Pa
     }
     if (e != cudaSuccess) return e;
     const int sms = current_device_sms();
-    const int grid = p.items < sms ? p.items : sms;
+    const int cap = p.max_ctas > 0 && p.max_ctas < sms ? p.max_ctas : sms;
+    const int grid = p.items < cap ? p.items : cap;
     const bool ragged = p.n % BN != 0;
     if constexpr (MODE == kModeCodes) {
-        if (causal && ragged)
+        if (p.ready != nullptr) {  // streamed step: non-causal, n % 128 == 0 only
+            if (causal || ragged) return cudaErrorInvalidValue;
+            e = smem_attr_once<int_flash_pp_kernel<D, false, MODE, false, true>>(smem);
+            if (e != cudaSuccess) return e;
+            int_flash_pp_kernel<D, false, MODE, false, true><<<grid, NUM_THREADS, smem, stream>>>(
+                tq, tk, tv, p);
+        } else if (causal && ragged)
             int_flash_pp_kernel<D, true, MODE, true><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
         else if (causal)
             int_flash_pp_kernel<D, true, MODE, false><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
@@ -906,6 +946,10 @@ static Params make_params(const float* sq, const float* sk, const float* sv, flo
     p.pairs = (q_tiles + 1) / 2;
     p.slices = static_cast<int32_t>(slices);
     p.items = p.pairs * p.slices;
+    p.ready = nullptr;
+    p.ready_target = 0;
+    p.ready_from = 0;
+    p.max_ctas = 0;
     return p;
 }
 
@@ -950,7 +994,11 @@ static cudaError_t launch(const AttnArgs& a, const uint16_t* v16_given, cudaStre
         p.o = o_even;
         p.o_pitch = static_cast<int32_t>(a.d + 1);
     }
-    if (int_flash_ws_enabled() || a.dump != nullptr)
+    p.ready = a.ready;
+    p.ready_target = a.ready_target;
+    p.ready_from = a.ready_from;
+    p.max_ctas = a.max_ctas;
+    if ((int_flash_ws_enabled() && a.ready == nullptr) || a.dump != nullptr)
         e = launch_int_flash_ws(a.q, a.sq, a.k, a.sk, reinterpret_cast<const uint16_t*>(v16), a.sv,
                                 p.o, a.slices, a.n, a.d, a.pitch, p.o_pitch, a.flags, a.dump,
                                 stream);

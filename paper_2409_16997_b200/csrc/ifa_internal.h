@@ -68,6 +68,12 @@ struct AttnArgs {
     int64_t bc;
     uint32_t flags;
     const AttnDump* dump = nullptr;  // tolerance-mode kernel only
+    // streamed step (attn_pp.cu only): wait for ready[slice] >= ready_target
+    // before reading a slice >= ready_from; grid capped at max_ctas (0 = all)
+    const uint32_t* ready = nullptr;
+    uint32_t ready_target = 0;
+    int32_t ready_from = 0;
+    int32_t max_ctas = 0;
 };
 
 // q/k/v rows have pitch `pitch` >= d with pitch % 16 == 0 (the C-ABI layer
@@ -85,6 +91,14 @@ cudaError_t launch_int_flash_pp(const AttnArgs& a, const uint16_t* v16, cudaStre
 // serves the S / P-code dumps).  v16 = [slices][n_pad][D] fp16 V codes (n_pad = n rounded up
 // to 128, zero rows past n), o rows of o_pitch floats.
 bool int_flash_ws_enabled();
+// quant.cu: Q, K per row and V per slice (+ fp16 V codes) of slices
+// [s0, slices), d in {64, 128}, on `ctas` CTAs that each own whole slices;
+// ready[s] = epoch (release) once slice s is complete.
+cudaError_t launch_stream_quantize(const float* q, const float* k, const float* v, int64_t s0,
+                                   int64_t slices, int64_t n, int64_t d, int8_t* qc, float* sq,
+                                   int8_t* kc, float* sk, int8_t* vc, float* sv, uint16_t* v16,
+                                   int64_t* bad, uint32_t* ready, uint32_t epoch, int ctas,
+                                   cudaStream_t stream);
 cudaError_t launch_int_flash_ws(const int8_t* q, const float* sq, const int8_t* k,
                                 const float* sk, const uint16_t* v16, const float* sv, float* o,
                                 int64_t slices, int64_t n, int64_t d, int64_t pitch,

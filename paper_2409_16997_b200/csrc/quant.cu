@@ -547,4 +547,191 @@ cudaError_t launch_fp8_quantize_per_tensor(const float* x, int64_t slices, int64
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------ streamed quantizer
+// Quantization of slices [s0, slices) on a few SMs next to the attention
+// kernel (ifa_int8_attention_step): CTA c owns whole slices s0 + c,
+// s0 + c + P, ... and streams each one start to end -- Q rows, K rows (8
+// lanes per row, 4 rows per warp step, two steps in flight), then V's abs
+// max and V's codes + fp16 codes (the second read hits L2) -- so every
+// pass is a long stream that keeps ~128 KB per SM in flight (measured
+// ~190 GB/s per SM for plain 128-bit loads, tools/microbench/sm_bw.cu).
+// When a slice is complete the CTA publishes ready[s] = epoch (release).
+// Arithmetic per element is exactly the per-row / per-tensor kernels'
+// (quant.cpp:25-69).
+template <int NV>
+__global__ void __launch_bounds__(1024, 1) stream_quantize_kernel(
+    const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
+    int64_t s0, int64_t slices, int64_t n, int8_t* __restrict__ qc, float* __restrict__ sq,
+    int8_t* __restrict__ kc, float* __restrict__ sk, int8_t* __restrict__ vc,
+    float* __restrict__ sv, uint16_t* __restrict__ v16, int64_t* bad, uint32_t* ready,
+    uint32_t epoch) {
+    constexpr int64_t D = 32 * NV;
+    const int lane = threadIdx.x & 31, l8 = lane & 7, warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    __shared__ float red[32];
+    __shared__ float s_max;
+
+    auto rows = [&](const float* x, int8_t* codes, float* scales, int64_t row0) {
+        // rows [row0, row0 + n) of x (flat row index, also the index base)
+        for (int64_t r0 = warp * 8; r0 < n; r0 += nwarps * 8) {
+            float4 val[2][NV];
+            int64_t rr[2];
+            bool ok[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                rr[h] = r0 + 4 * h + (lane >> 3);
+                ok[h] = rr[h] < n;
+                const float4* src = reinterpret_cast<const float4*>(x + (row0 + rr[h]) * D);
+#pragma unroll
+                for (int j = 0; j < NV; ++j)
+                    val[h][j] = ok[h] ? __ldcs(src + l8 + 8 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float m = 0.0f;
+#pragma unroll
+                for (int j = 0; j < NV; ++j)
+                    m = absmax_nan(absmax_nan(m, val[h][j].x, val[h][j].y), val[h][j].z,
+                                   val[h][j].w);
+#pragma unroll
+                for (int o = 4; o > 0; o >>= 1) {
+                    const float other = __shfl_xor_sync(0xffffffffu, m, o);
+                    asm("max.NaN.f32 %0, %0, %1;" : "+f"(m) : "f"(other));
+                }
+                const int64_t row = row0 + rr[h];
+                if (!(m <= 3.402823466e38f) && ok[h]) {  // locate the non-finite input
+#pragma unroll
+                    for (int j = 0; j < NV; ++j) {
+                        const int64_t b = row * D + 4 * (l8 + 8 * j);
+                        note_nonfinite(val[h][j].x, b + 0, bad);
+                        note_nonfinite(val[h][j].y, b + 1, bad);
+                        note_nonfinite(val[h][j].z, b + 2, bad);
+                        note_nonfinite(val[h][j].w, b + 3, bad);
+                    }
+                }
+                const float scale = __fdiv_rn(m, 127.0f);
+                const float rcp = __frcp_rn(scale);
+                const bool exact_row = !(rcp <= 3.402823466e38f);
+                if (ok[h]) {
+                    if (l8 == 0) scales[row] = scale;
+                    uint32_t* dst = reinterpret_cast<uint32_t*>(codes + row * D);
+#pragma unroll
+                    for (int j = 0; j < NV; ++j)
+                        dst[l8 + 8 * j] = codes4(val[h][j], scale, rcp, exact_row);
+                }
+            }
+        }
+    };
+    const int64_t E4 = n * D / 4;  // float4 per slice
+    for (int64_t s = s0 + blockIdx.x; s < slices; s += gridDim.x) {
+        rows(q, qc, sq, s * n);
+        rows(k, kc, sk, s * n);
+        // V: abs max of the slice
+        const float4* src = reinterpret_cast<const float4*>(v + s * n * D);
+        float m = 0.0f;
+        {
+            const int64_t stride = blockDim.x;
+            int64_t i = threadIdx.x;
+            for (; i + 3 * stride < E4; i += 4 * stride) {
+                const float4 a = src[i], b = src[i + stride], c = src[i + 2 * stride],
+                             d = src[i + 3 * stride];
+                m = absmax_nan(absmax_nan(m, a.x, a.y), a.z, a.w);
+                m = absmax_nan(absmax_nan(m, b.x, b.y), b.z, b.w);
+                m = absmax_nan(absmax_nan(m, c.x, c.y), c.z, c.w);
+                m = absmax_nan(absmax_nan(m, d.x, d.y), d.z, d.w);
+            }
+            for (; i < E4; i += stride) {
+                const float4 a = src[i];
+                m = absmax_nan(absmax_nan(m, a.x, a.y), a.z, a.w);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float other = __shfl_xor_sync(0xffffffffu, m, o);
+            asm("max.NaN.f32 %0, %0, %1;" : "+f"(m) : "f"(other));
+        }
+        if (lane == 0) red[warp] = m;
+        __syncthreads();
+        if (warp == 0) {
+            float x = lane < nwarps ? red[lane] : 0.0f;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float other = __shfl_xor_sync(0xffffffffu, x, o);
+                asm("max.NaN.f32 %0, %0, %1;" : "+f"(x) : "f"(other));
+            }
+            if (lane == 0) s_max = x;
+        }
+        __syncthreads();
+        const float smax = s_max;
+        const float scale = __fdiv_rn(smax, 127.0f);
+        if (threadIdx.x == 0) sv[s] = scale;
+        if (!(smax <= 3.402823466e38f)) {
+            for (int64_t i = threadIdx.x; i < E4; i += blockDim.x) {
+                const float4 a = src[i];
+                const int64_t b = s * n * D + 4 * i;
+                note_nonfinite(a.x, b + 0, bad);
+                note_nonfinite(a.y, b + 1, bad);
+                note_nonfinite(a.z, b + 2, bad);
+                note_nonfinite(a.w, b + 3, bad);
+            }
+        }
+        const float rcp = __frcp_rn(scale);
+        const bool exact_row = !(rcp <= 3.402823466e38f);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(vc + s * n * D);
+        uint2* dst16 = reinterpret_cast<uint2*>(v16 + s * n * D);
+        {
+            const int64_t stride = blockDim.x;
+            int64_t i = threadIdx.x;
+            for (; i + 3 * stride < E4; i += 4 * stride) {
+                const float4 a = __ldcs(src + i), b = __ldcs(src + i + stride),
+                             c = __ldcs(src + i + 2 * stride), d = __ldcs(src + i + 3 * stride);
+                const uint32_t wa = codes4(a, scale, rcp, exact_row);
+                const uint32_t wb = codes4(b, scale, rcp, exact_row);
+                const uint32_t wc = codes4(c, scale, rcp, exact_row);
+                const uint32_t wd = codes4(d, scale, rcp, exact_row);
+                dst[i] = wa;
+                dst[i + stride] = wb;
+                dst[i + 2 * stride] = wc;
+                dst[i + 3 * stride] = wd;
+                dst16[i] = codes4_to_f16(wa);
+                dst16[i + stride] = codes4_to_f16(wb);
+                dst16[i + 2 * stride] = codes4_to_f16(wc);
+                dst16[i + 3 * stride] = codes4_to_f16(wd);
+            }
+            for (; i < E4; i += stride) {
+                const uint32_t w = codes4(__ldcs(src + i), scale, rcp, exact_row);
+                dst[i] = w;
+                dst16[i] = codes4_to_f16(w);
+            }
+        }
+        __syncthreads();  // the whole slice is written
+        if (threadIdx.x == 0) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ready + s), "r"(epoch)
+                         : "memory");
+        }
+    }
+}
+
+cudaError_t launch_stream_quantize(const float* q, const float* k, const float* v, int64_t s0,
+                                   int64_t slices, int64_t n, int64_t d, int8_t* qc, float* sq,
+                                   int8_t* kc, float* sk, int8_t* vc, float* sv, uint16_t* v16,
+                                   int64_t* bad, uint32_t* ready, uint32_t epoch, int ctas,
+                                   cudaStream_t stream) {
+    if (d != 64 && d != 128) return cudaErrorInvalidValue;
+    const uintptr_t al = reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) |
+                         reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(qc) |
+                         reinterpret_cast<uintptr_t>(kc) | reinterpret_cast<uintptr_t>(vc) |
+                         reinterpret_cast<uintptr_t>(v16);
+    if (al % 16 != 0 || ctas < 1) return cudaErrorInvalidValue;
+    if (s0 >= slices) return cudaSuccess;
+    if (d == 128)
+        stream_quantize_kernel<4><<<ctas, 1024, 0, stream>>>(q, k, v, s0, slices, n, qc, sq, kc,
+                                                             sk, vc, sv, v16, bad, ready, epoch);
+    else
+        stream_quantize_kernel<2><<<ctas, 1024, 0, stream>>>(q, k, v, s0, slices, n, qc, sq, kc,
+                                                             sk, vc, sv, v16, bad, ready, epoch);
+    return cudaGetLastError();
+}
+
 }  // namespace ifa_b200

@@ -53,6 +53,13 @@ class AttentionPlan:
             if self.uses_pp_kernel() and d in (64, 128) and n % 128 == 0 else None
         # V (two passes + a cluster sync per slice) runs on a side stream next to
         # the single-pass Q/K row kernels, so HBM stays busy through V's syncs
+        # streamed step (ifa_int8_attention_step): per-slice ready counters
+        self._sync = torch.zeros((2 * slices,), dtype=torch.int32, device=dev) \
+            if self.v16 is not None else None
+        self._epoch = 0
+        # off by default: measured slower than quantize-then-attention on C2 and
+        # C5; IFA_B200_STREAMED=1 selects it
+        self.streamed = self.v16 is not None and os.environ.get("IFA_B200_STREAMED", "0") == "1"
         self._side = torch.cuda.Stream(dev)
         self._fork = torch.cuda.Event()
         self._join = torch.cuda.Event()
@@ -108,8 +115,29 @@ class AttentionPlan:
                     tuple(t.shape) != (self.slices, self.n, self.d) or t.device != self.device:
                 raise ValueError("AttentionPlan.forward: expected contiguous f32 "
                                  f"{(self.slices, self.n, self.d)} tensors on {self.device}")
+        if self.streamed:
+            return self.step(q, k, v, stream)
         self.quantize(q, k, v, stream)
         return self.attention(stream)
+
+    def step(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+             stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """The whole step as one ifa_int8_attention_step call: the quantizer
+        runs on a few SMs next to the attention kernel, which waits per slice
+        (same results as quantize() + attention())."""
+        assert self._sync is not None, "step() needs the fp16-V (two-Q-tile) configuration"
+        s = int((stream or torch.cuda.current_stream(self.device)).cuda_stream)
+        self._epoch += 1
+        if self._epoch >= 1 << 31:  # the ready words hold the epoch
+            self._sync.zero_()
+            self._epoch = 1
+        _lib.check(self.lib.ifa_int8_attention_step(
+            q.data_ptr(), k.data_ptr(), v.data_ptr(), self.qc.data_ptr(), self.sq.data_ptr(),
+            self.kc.data_ptr(), self.sk.data_ptr(), self.vc.data_ptr(), self.sv.data_ptr(),
+            self.v16.data_ptr(), self.out.data_ptr(), self.bad.data_ptr(),
+            self._sync.data_ptr(), self._epoch, self.slices, self.n, self.d, self.br, self.bc,
+            self.flags, s))
+        return self.out
 
     def uses_pp_kernel(self) -> bool:
         """True when ifa_int_flash_fwd takes the two-Q-tile tolerance kernel
@@ -125,6 +153,8 @@ class AttentionPlan:
         slices -- or absmax + quantize + a memset on shapes the fused V
         kernel does not take; attention: one persistent kernel, plus the V
         fp16 conversion on the two-Q-tile path)."""
+        if self.streamed:
+            return 5  # first slices: Q rows, K rows, V; stream quantizer; attention
         elems = self.n * self.d
         v_fused = elems % 16 == 0 and self.d % 4 == 0
         pp = self.uses_pp_kernel()
@@ -143,12 +173,16 @@ class AttentionPlan:
         """Record forward(q, k, v) into a CUDA graph (replay with ``replay()``)."""
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
+        # a graph replays fixed kernel arguments, so the streamed step (whose
+        # epoch advances every call) is not captured: quantize + attention
         with torch.cuda.stream(s):
-            self.forward(q, k, v, s)  # warm-up outside the graph (lazy init)
+            self.quantize(q, k, v, s)  # warm-up outside the graph (lazy init)
+            self.attention(s)
         torch.cuda.current_stream(self.device).wait_stream(s)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self.forward(q, k, v)
+            self.quantize(q, k, v)
+            self.attention()
         self.graph = g
         self._graph_io = (q, k, v)
 

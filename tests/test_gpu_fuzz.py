@@ -9,7 +9,7 @@ import torch
 
 pytestmark = pytest.mark.gpu
 
-FAST_MRE = 5e-5
+FAST_MRE = 5e-5  # random shapes down to n = 1 (few keys per row); fixed shapes hold 2e-5
 
 
 def _case(seed):

@@ -251,10 +251,12 @@ def test_validation_errors(ifa):
 # exactness guard.  Codes/scales/S are exact by construction (same quantize
 # kernels, same integer GEMM); O is held to the stated tolerance against the
 # exact reference result:
-#   MRE (normalized L1, eval.cpp:55-75) <= 5e-5, and
+#   MRE (normalized L1, eval.cpp:55-75) <= 2e-5 (measured worst 1.28e-5 over
+#   every case below, bc = 200 on the 16-warp kernel; 7.7e-7 on C2 slices;
+#   the long-sequence / dump / host tests hold 1e-5), and
 #   max|dO| <= 2/127 * max|V_code| * sV   (the reference's own multi-block
 #   bound, verify.cpp:65-70).
-FAST_MRE = 5e-5
+FAST_MRE = 2e-5
 
 
 def _fast_close(got, want, vc, vs):
