@@ -2,6 +2,14 @@
 // code_bounds.h).  The double-precision steps are written with explicit
 // std::fma where glibc's FMA variant contracts and volatile temporaries
 // where it does not, so the result does not depend on host compiler flags.
+//
+// Provenance: the 32-entry 2^(i/32) table and the polynomial / shift
+// constants are glibc's __exp2f_data (sysdeps/ieee754/flt-32/e_exp2f_data.c,
+// glibc 2.39), which comes from ARM's optimized-routines (MIT OR Apache-2.0
+// WITH LLVM-exception; glibc ships it under LGPL-2.1+).  They are
+// mathematical constants reproduced because bit-exact parity with the
+// reference's libm expf needs exactly these values; no code is copied from
+// the reference (which has none of it) or from glibc.
 #include "code_bounds.h"
 
 #include <cmath>

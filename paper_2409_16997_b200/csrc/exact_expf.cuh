@@ -8,6 +8,14 @@
 // __fma_rn so the result is bit-identical to the host routine; the
 // identical C restatement (oracle/ifa_oracle.c: ifa_or_expf) matched the
 // container's libm on all 2,239,627,266 floats in [-103, 88].
+//
+// Provenance: the 32-entry 2^(i/32) table and the polynomial / shift
+// constants are glibc's __exp2f_data (sysdeps/ieee754/flt-32/e_exp2f_data.c,
+// glibc 2.39), which comes from ARM's optimized-routines (MIT OR Apache-2.0
+// WITH LLVM-exception; glibc ships it under LGPL-2.1+).  They are
+// mathematical constants reproduced because bit-exact parity with the
+// reference's libm expf needs exactly these values; no code is copied from
+// the reference (which has none of it) or from glibc.
 #pragma once
 #include <cstdint>
 
