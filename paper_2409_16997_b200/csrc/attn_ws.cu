@@ -108,6 +108,22 @@ constexpr bool kNamedMsg = IFA_WS_NAMED_MSG != 0;
 // 7 + 2g + slot message empty (softmax warpgroup g + correction warpgroup)
 __host__ __device__ constexpr uint32_t msg_full_id(uint32_t g, uint32_t slot) { return 3 + 2 * g + slot; }
 __host__ __device__ constexpr uint32_t msg_empty_id(uint32_t g, uint32_t slot) { return 7 + 2 * g + slot; }
+// Cold-code skipping (see attn_pp.cu IFA_PP_SPARSE): in the one-row-per-
+// thread layout the exp2 phase is MUFU-bound (tools/microbench/code_loop.cu:
+// 1194 clk per 128-key row, floor 1024), and a MUFU warp-instruction costs
+// its pipe time even with every lane off, so whole 8-key chunks are skipped
+// by a warp vote when none of the warp's 32 rows needs a nonzero code
+// there.  Used when at most IFA_WS_SPARSE_HOT rows of the warp reach t > -1
+// in this block; otherwise the dense loop runs.  Results are identical.
+// Measured OFF: C2 1.090 -> 1.225 ms (normal), 1.161 ms (uniform): the exp2
+// phase is not what bounds this kernel's period once it runs next to the
+// other group's dequant phase.
+#ifndef IFA_WS_SPARSE
+#define IFA_WS_SPARSE 0
+#endif
+#ifndef IFA_WS_SPARSE_HOT
+#define IFA_WS_SPARSE_HOT 16
+#endif
 #ifndef IFA_WS_CORR_SLEEP_NS
 #define IFA_WS_CORR_SLEEP_NS 0
 #endif
@@ -764,6 +780,55 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     // exact, so one PRMT packs two codes.  The row sum adds the
                     // packed words as integers (<= 64 * 127 per half).
                     uint32_t acc = 0u;
+                    const float tmax = __fmaf_rn(sq, b, cr);  // the row's largest exponent
+                    const bool sparse =
+                        IFA_WS_SPARSE &&
+                        __popc(__ballot_sync(0xffffffffu, !(tmax < -1.0f))) <= IFA_WS_SPARSE_HOT;
+                    auto store_chunk = [&](int ch, const uint32_t (&wd)[4]) {
+                        const uint32_t chunk = (static_cast<uint32_t>(ch & 7) ^ sw);
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                         p_row + (ch >> 3) * (BM * 128) + chunk * 16),
+                                     "r"(wd[0]), "r"(wd[1]), "r"(wd[2]), "r"(wd[3])
+                                     : "memory");
+                        if (DUMP && p.p_dump != nullptr && grow < n) {
+                            uint8_t* dst = p.p_dump + (static_cast<int64_t>(slice) * n + grow) * n + j * BN + 8 * ch;
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                if (j * BN + 8 * ch + 2 * e < n) dst[2 * e] = static_cast<uint8_t>(wd[e] & 0xffu);
+                                if (j * BN + 8 * ch + 2 * e + 1 < n)
+                                    dst[2 * e + 1] = static_cast<uint8_t>((wd[e] >> 16) & 0xffu);
+                            }
+                        }
+                    };
+                    if (sparse) {
+                        // per 8-key chunk: exponents, a warp vote, exp2 only when
+                        // some row of the warp has a nonzero code there
+#pragma unroll
+                        for (int ch = 0; ch < 16; ++ch) {
+                            float2 t[4];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                t[e] = ffma2(make_float2(u[8 * ch + 2 * e], u[8 * ch + 2 * e + 1]), f2(sq),
+                                             f2(cr));
+                            const float tm = fmaxf(fmax3(t[0].x, t[0].y, t[1].x),
+                                                   fmax3(fmax3(t[1].y, t[2].x, t[2].y), t[3].x, t[3].y));
+                            uint32_t wd[4] = {0u, 0u, 0u, 0u};
+                            if (__any_sync(0xffffffffu, tm >= -1.0f)) {
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    float2 c = fadd2(make_float2(ex2(t[e].x), ex2(t[e].y)), f2(kMagic));
+                                    if (dmask) {
+                                        if (8 * ch + 2 * e > kmax) c.x = kMagic;
+                                        if (8 * ch + 2 * e + 1 > kmax) c.y = kMagic;
+                                    }
+                                    wd[e] = prmt(__float_as_uint(c.x), __float_as_uint(c.y), 0x5410u);
+                                }
+                                acc += wd[0] + wd[1];
+                                acc += wd[2] + wd[3];
+                            }
+                            store_chunk(ch, wd);
+                        }
+                    } else {
                     // all 128 exp2 first (in place of u), then the rounding and
                     // packing, chunk c's magic add made to depend on an exp2
                     // result kLag pairs further on: otherwise ptxas puts each
@@ -809,6 +874,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                     dst[2 * e + 1] = static_cast<uint8_t>((wd[e] >> 16) & 0xffu);
                             }
                         }
+                    }
                     }
                     fence_proxy_async_shared();  // P is read by the tensor core
                     __syncwarp();
