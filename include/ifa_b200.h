@@ -106,7 +106,8 @@ int ifa_int_flash_fwd(const int8_t* q, const float* sq, const int8_t* k, const f
 /* ---- int32 S / P-code dump (north_star: "int32 S tiles bit-exact") --------
  * ifa_int_flash_fwd_dump: ifa_int_flash_fwd in tolerance mode (flags must
  *   hold IFA_FLAG_FAST; Bc = 128, or Bc >= n <= 128) through a separate
- *   instantiation of the full-INT8 tolerance kernel that also writes
+ *   instantiation of the bench-default full-INT8 tolerance kernel
+ *   (csrc/attn_pp.cu; csrc/attn_ws.cu with IFA_B200_WS=1) that also writes
  *     s_out   [slices][n][n] int32: S = Q.K^T of every KV tile the kernel
  *             computes, read back from the tcgen05 kind::i8 accumulator in
  *             TMEM -- the reference's int_gemm_nt_strided

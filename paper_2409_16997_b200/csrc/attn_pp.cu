@@ -133,6 +133,9 @@ struct Params {
     uint32_t ready_target;
     int32_t ready_from;  // slices below it were quantized before the launch
     int32_t max_ctas;    // grid cap (SMs left to the quantizer), 0 = all SMs
+    // DUMP instantiation only: [slices][n][n] int32 S and uint8 P codes
+    int32_t* s_dump;
+    uint8_t* p_dump;
 };
 
 // Waits until the quantizer has published slice `slice` (acquire), then
@@ -276,7 +279,9 @@ __device__ __forceinline__ void mma_f8_ss(uint32_t d_tmem, uint64_t a_desc, uint
 // a template parameter so the common case carries no masking code.
 // STREAMED: the inputs of a slice are waited for per item (streamed step); a
 // separate instantiation because the check costs the math warps registers.
-template <int D, bool CAUSAL, int MODE, bool RAGGED, bool STREAMED = false>
+// DUMP: also write S and the P codes to p.s_dump / p.p_dump (parity checks;
+// a separate instantiation, so the product kernel carries no dump code).
+template <int D, bool CAUSAL, int MODE, bool RAGGED, bool STREAMED = false, bool DUMP = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     int_flash_pp_kernel(const __grid_constant__ CUtensorMap tm_q,
                         const __grid_constant__ CUtensorMap tm_k,
@@ -558,6 +563,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) ld16x256_x4(t_s + 32 * c, &sr[16 * c]);
                 tmem_wait_ld();
+                if constexpr (DUMP) {  // sr[4k + 2r + e]: row row0 + 8r, key 8k + 2 t0 + e
+                    if (p.s_dump != nullptr) {
+#pragma unroll
+                        for (int r = 0; r < 2; ++r) {
+                            if (grow[r] >= n) continue;
+                            int32_t* dst = p.s_dump + (static_cast<int64_t>(slice) * n + grow[r]) * n;
+#pragma unroll
+                            for (int k = 0; k < 16; ++k)
+#pragma unroll
+                                for (int e = 0; e < 2; ++e) {
+                                    const int32_t key = j * BN + 8 * k + 2 * static_cast<int32_t>(t0) + e;
+                                    if (key < n) dst[key] = static_cast<int32_t>(sr[4 * k + 2 * r + e]);
+                                }
+                        }
+                    }
+                }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) bar_arrive(bs_empty);
@@ -715,6 +736,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                         for (int r = 0; r < 2; ++r)
                             lsum[r] = static_cast<float>(static_cast<int32_t>((acc[r] & 0xffffu) + (acc[r] >> 16)));
+                        if constexpr (DUMP) {  // wd[r][k]: codes of keys 8k + 2 t0 + {0, 1} (low bytes)
+                            if (p.p_dump != nullptr) {
+#pragma unroll
+                                for (int r = 0; r < 2; ++r) {
+                                    if (grow[r] >= n) continue;
+                                    uint8_t* dst = p.p_dump + (static_cast<int64_t>(slice) * n + grow[r]) * n;
+#pragma unroll
+                                    for (int k = 0; k < 16; ++k) {
+                                        const int32_t key = j * BN + 8 * k + 2 * static_cast<int32_t>(t0);
+                                        if (key < n) dst[key] = static_cast<uint8_t>(wd[r][k] & 0xffu);
+                                        if (key + 1 < n) dst[key + 1] = static_cast<uint8_t>((wd[r][k] >> 16) & 0xffu);
+                                    }
+                                }
+                            }
+                        }
                     } else {
                         // half-INT8 / FP8: the float weights, rounded to fp16
                         float2 ls[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
@@ -956,7 +992,20 @@ static cudaError_t run(const void* q, const void* k, const __half* v16, const Pa
     const int grid = p.items < cap ? p.items : cap;
     const bool ragged = p.n % BN != 0;
     if constexpr (MODE == kModeCodes) {
-        if (p.ready != nullptr) {  // streamed step: non-causal, n % 128 == 0 only
+        if (p.s_dump != nullptr || p.p_dump != nullptr) {  // parity dumps: the ragged-capable code
+            if (causal) {
+                e = smem_attr_once<int_flash_pp_kernel<D, true, MODE, true, false, true>>(smem);
+                if (e == cudaSuccess)
+                    int_flash_pp_kernel<D, true, MODE, true, false, true>
+                        <<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+            } else {
+                e = smem_attr_once<int_flash_pp_kernel<D, false, MODE, true, false, true>>(smem);
+                if (e == cudaSuccess)
+                    int_flash_pp_kernel<D, false, MODE, true, false, true>
+                        <<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+            }
+            if (e != cudaSuccess) return e;
+        } else if (p.ready != nullptr) {  // streamed step: non-causal, n % 128 == 0 only
             if (causal || ragged) return cudaErrorInvalidValue;
             e = smem_attr_once<int_flash_pp_kernel<D, false, MODE, false, true>>(smem);
             if (e != cudaSuccess) return e;
@@ -997,6 +1046,8 @@ static Params make_params(const float* sq, const float* sk, const float* sv, flo
     p.ready_target = 0;
     p.ready_from = 0;
     p.max_ctas = 0;
+    p.s_dump = nullptr;
+    p.p_dump = nullptr;
     return p;
 }
 
@@ -1045,7 +1096,12 @@ static cudaError_t launch(const AttnArgs& a, const uint16_t* v16_given, cudaStre
     p.ready_target = a.ready_target;
     p.ready_from = a.ready_from;
     p.max_ctas = a.max_ctas;
-    if ((int_flash_ws_enabled() && a.ready == nullptr) || a.dump != nullptr)
+    if (a.dump != nullptr && !int_flash_ws_enabled()) {
+        p.s_dump = a.dump->s;
+        p.p_dump = a.dump->p;
+    }
+    if ((int_flash_ws_enabled() && a.ready == nullptr) ||
+        (a.dump != nullptr && int_flash_ws_enabled()))
         e = launch_int_flash_ws(a.q, a.sq, a.k, a.sk, reinterpret_cast<const uint16_t*>(v16), a.sv,
                                 p.o, a.slices, a.n, a.d, a.pitch, p.o_pitch, a.flags, a.dump,
                                 stream);

@@ -87,8 +87,8 @@ bool int_flash_pp_eligible(const AttnArgs& a);
 // 128), or null to convert a.v internally.
 cudaError_t launch_int_flash_pp(const AttnArgs& a, const uint16_t* v16, cudaStream_t stream);
 // attn_ws.cu: the full-INT8 tolerance-mode kernel with one softmax thread
-// per row (IFA_B200_WS=1 selects it for int_flash_pp_eligible calls, and it
-// serves the S / P-code dumps).  v16 = [slices][n_pad][D] fp16 V codes (n_pad = n rounded up
+// per row (IFA_B200_WS=1 selects it for int_flash_pp_eligible calls and for
+// the S / P-code dumps, which otherwise run on attn_pp.cu's DUMP kernel).  v16 = [slices][n_pad][D] fp16 V codes (n_pad = n rounded up
 // to 128, zero rows past n), o rows of o_pitch floats.
 bool int_flash_ws_enabled();
 // quant.cu: Q, K per row and V per slice (+ fp16 V codes) of slices

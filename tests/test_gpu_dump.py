@@ -1,9 +1,11 @@
 """int32 S tiles and P codes of the tolerance-mode kernel vs the reference.
 
 north_star: "int32 S tiles bit-exact".  ``ifa_int_flash_fwd_dump`` runs a
-separate instantiation of the full-INT8 tolerance kernel (csrc/attn_ws.cu)
-that writes every S tile it reads back from the tcgen05 kind::i8 TMEM
-accumulator, and every P code it feeds to P.V.
+separate instantiation of the full-INT8 tolerance kernel -- the bench-default
+two-Q-tile kernel (csrc/attn_pp.cu), or with IFA_B200_WS=1 the
+one-row-per-thread kernel (csrc/attn_ws.cu); both are tested -- that writes
+every S tile it reads back from the tcgen05 kind::i8 TMEM accumulator, and
+every P code it feeds to P.V.
 
 * S is compared BITWISE with the oracle's int_gemm_nt (gemm.cpp:32-46,
   reached from attention.cpp:275-276), with the unmodified reference
@@ -23,6 +25,12 @@ import pytest
 import torch
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(params=["pp", "ws"], autouse=True)
+def kernel(request, monkeypatch):
+    monkeypatch.setenv("IFA_B200_WS", "1" if request.param == "ws" else "0")
+    return request.param
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "c1_known_answers.json")
 MAX_FLIP_RATE = 1e-4
