@@ -64,7 +64,7 @@ def kernels(lib=LIB):
 
 def family(name):
     if "int_flash_pp_kernel" in name:
-        mode = re.search(r"<\d+, \w+, (\d), \w+(, \w+)?>", name)
+        mode = re.search(r"<\d+, \w+, (\d), \w+(, \w+)*>", name)
         return {"0": "pp full-INT8 (tolerance, bench default)", "1": "pp half-INT8",
                 "2": "pp FP8"}[mode.group(1)] if mode else "pp"
     if "int_flash_ws_kernel" in name:
