@@ -602,13 +602,19 @@ def main() -> None:
         # metric is a rate, so a subset of the workload measures it)
         e2e_slices = min(slices, 256)
         try:
-            line["e2e"] = e2e_cabi_run(torch, e2e_slices, N, d, bc, causal,
-                                       args.mode == "fast", dev,
-                                       e2e_slices * attn_ops(N, d, causal), args.steps)
+            line["e2e"] = e2e_plugin_run(torch, plan, e2e_slices, N, d, bc, causal,
+                                         args.mode == "fast", dev,
+                                         e2e_slices * attn_ops(N, d, causal), args.steps)
             if e2e_slices != slices:
                 line["e2e"]["sample"] = f"{e2e_slices} of the rank's {slices} slices"
         except Exception as e:  # pragma: no cover
             line["e2e"] = {"error": str(e)[:200]}
+        try:
+            line["e2e_full_step"] = e2e_cabi_run(torch, e2e_slices, N, d, bc, causal,
+                                                 args.mode == "fast", dev,
+                                                 e2e_slices * attn_ops(N, d, causal), args.steps)
+        except Exception as e:  # pragma: no cover
+            line["e2e_full_step"] = {"error": str(e)[:200]}
         try:
             line["e2e_python"] = e2e_run(torch, e2e_slices, N, d, bc, causal,
                                          args.mode == "fast", dev,
@@ -765,6 +771,46 @@ def verify_ranks(torch, dist, plan, q, k, v, slices, N, d, bc, causal, fast, wor
         "all_ok": all(p[key] for p in per_rank),
     }
     return out
+
+
+def e2e_plugin_run(torch, plan, slices, N, d, bc, causal, fast, dev, ops_rank, steps) -> dict:
+    """The metric end to end through the reference-facing plugin path: the
+    host-buffer twin of IntFlashFn (verify.hpp:15-16, what
+    ifa_gpu::int_flash_attention[_fast] calls) -- ifa_int_flash_fwd_host:
+    int8 codes + scales of Q, K, V in pinned host memory (the quantized
+    inputs the reference's int_flash_attention takes, attention.hpp:85-87)
+    -> GPU -> f32 O in host memory, chunk-pipelined over three streams inside
+    the library.  Synchronous, so timed with the host clock around it."""
+    import ctypes as C
+    from paper_2409_16997_b200 import _lib
+    lib = _lib.load()
+    hq, hk, hv = (t[:slices].cpu().pin_memory() for t in (plan.qc, plan.kc, plan.vc))
+    hsq, hsk, hsv = (t[:slices].cpu().pin_memory() for t in (plan.sq, plan.sk, plan.sv))
+    ho = torch.empty((slices, N, d), dtype=torch.float32).pin_memory()
+    flags = (_lib.FLAG_FAST if fast else 0) | (_lib.FLAG_CAUSAL if causal else 0)
+    ptr = lambda t: C.c_void_p(t.data_ptr())
+
+    def call():
+        _lib.check(lib.ifa_int_flash_fwd_host(ptr(hq), ptr(hsq), ptr(hk), ptr(hsk), ptr(hv),
+                                              ptr(hsv), ptr(ho), slices, N, d, 128, bc, flags,
+                                              None, None))
+
+    call()
+    torch.cuda.synchronize(dev)
+    n_steps = max(2, min(steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(n_steps):
+        call()
+    dt = (time.perf_counter() - t0) / n_steps
+    h2d = sum(t.numel() * t.element_size() for t in (hq, hk, hv, hsq, hsk, hsv))
+    return {"value": ops_rank / dt / 1e12, "unit": "TOPS",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": ho.numel() * 4,
+            "ms_per_step": dt * 1e3, "steps": n_steps,
+            "path": "ifa_int_flash_fwd_host (C-ABI twin of the reference's IntFlashFn plugin, "
+                    "verify.hpp:15-16): pinned host int8 codes + scales -> chunked 3-stream "
+                    "H2D / attention kernel / D2H inside libifa_b200.so -> host f32 O; "
+                    "host-clock timed (the reference arm times int_flash_attention on the same "
+                    "quantized inputs)"}
 
 
 def e2e_cabi_run(torch, slices, N, d, bc, causal, fast, dev, ops_rank, steps) -> dict:
