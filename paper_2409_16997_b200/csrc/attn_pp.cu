@@ -138,6 +138,22 @@ struct Params {
     uint8_t* p_dump;
 };
 
+// -DIFA_PP_TRACE=1 (tools/build_variant.sh): clock64 stamps of CTA 0's
+// pipeline events, read back with ifa_pp_trace_read (tools/pp_trace.py).
+// role 0 = math warp 4 + 8g (rows 0-15 of group g), role 1 = MMA issuer g.
+#ifdef IFA_PP_TRACE
+__device__ unsigned long long g_pp_trace[2 * 2 * 1024 * 8];
+#define PP_TR(role, g, t, ev)                                                             \
+    do {                                                                                 \
+        if (blockIdx.x == 0 && (t) < 1024)                                               \
+            g_pp_trace[(((role) * 2 + (g)) * 1024 + (t)) * 8 + (ev)] = clock64();        \
+    } while (0)
+#else
+#define PP_TR(role, g, t, ev) \
+    do {                      \
+    } while (0)
+#endif
+
 // Waits until the quantizer has published slice `slice` (acquire), then
 // orders this thread's later async-proxy (TMA) reads after it.  Traps after
 // ~4 s instead of hanging (a quantizer that cannot make progress).
@@ -469,10 +485,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             for (int32_t a = 0; a < ahead; ++a) nk.advance();
                             bar_wait(b_s_empty + 8 * g, t & 1);
                             issue_s(nk.idx, nk.phase);
+                            PP_TR(1, g, t, 0);
                         }
                         bar_wait(b_v_full + 8 * vr.idx, vr.phase);
                         const uint32_t v_base = smem_u32(sm.v[vr.idx]);
                         bar_wait(b_p_full + 8 * g, t & 1);
+                        PP_TR(1, g, t, 1);
                         if (j == 0 && wi > 0) bar_wait(b_o_free + 8 * g, (wi - 1) & 1);
                         tc_fence_after();
 #pragma unroll
@@ -485,6 +503,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             mma_f16_ss(d_o, adesc, bdesc, kIdescPV, (j == 0 && kk == 0) ? 0u : 1u);
                         }
                         mma_commit_u32(b_p_empty + 8 * g);
+                        PP_TR(1, g, t, 2);
                         if (last) mma_commit_u32(b_o_full + 8 * g);
                         mma_commit_u32(b_v_empty + 8 * vr.idx);
                         kr.advance();
@@ -557,7 +576,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     kv.advance();
                     continue;
                 }
+                const bool tr = (mw & 7) == 0 && lane == 0;
+                if (tr) PP_TR(0, g, tc, 7);
                 bar_wait(bs_full, tc & 1);
+                if (tr) PP_TR(0, g, tc, 0);
                 tc_fence_after();
                 uint32_t sr[64];
 #pragma unroll
@@ -582,6 +604,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) bar_arrive(bs_empty);
+                if (tr) PP_TR(0, g, tc, 1);
                 bar_wait(b_k_full + 8 * st, kv.phase);
                 // u = float(S) * sK * log2(e); sr[4k + {0,1}] row0, [4k + {2,3}] row1,
                 // keys 8k + 2*t0 + {0,1}
@@ -657,6 +680,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         alpha[r] = (j == 0 || mnew == m[r]) ? 1.0f : ex2(sq[r] * (m[r] - mnew));
                         m[r] = mnew;
                     }
+                    if (tr) PP_TR(0, g, tc, 2);
                     // weights: 6 of 8 exp2 on MUFU, 2 on the FMA pipe.
                     // wd[r][k] = keys (8k + 2t0, +1) of row r as fp16x2.
                     uint32_t wd[2][16];
@@ -675,6 +699,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     if constexpr (early_p) {
                         // P.V(j-1) has long finished by now: P is stored as it is made
                         if (tc > 0) bar_wait(bp_empty, (tc - 1) & 1);
+                        if (tr) PP_TR(0, g, tc, 3);
                         tc_fence_after();
                     }
                     if constexpr (MODE == kModeCodes) {
@@ -784,6 +809,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         if (tc > 0) bar_wait(bp_empty, (tc - 1) & 1);
                         tc_fence_after();
                     }
+                    if (tr) PP_TR(0, g, tc, 4);
                     const bool need = j > 0 && (alpha[0] != 1.0f || alpha[1] != 1.0f);
                     if (__any_sync(0xffffffffu, need)) {
     #pragma unroll
@@ -815,6 +841,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) bar_arrive(bp_full);
+                    if (tr) PP_TR(0, g, tc, 5);
 
 #pragma unroll
                     for (int r = 0; r < 2; ++r) l[r] = __fmaf_rn(l[r], alpha[r], lsum[r]);
@@ -1119,6 +1146,15 @@ static cudaError_t launch(const AttnArgs& a, const uint16_t* v16_given, cudaStre
 }
 
 }  // namespace pp
+
+#ifdef IFA_PP_TRACE
+extern "C" int ifa_pp_trace_read(unsigned long long* host, int64_t count) {
+    return cudaMemcpyFromSymbol(host, pp::g_pp_trace, sizeof(unsigned long long) * count) ==
+                   cudaSuccess
+               ? 0
+               : 1;
+}
+#endif
 
 bool int_flash_pp_eligible(const AttnArgs& a) {
     const char* off = std::getenv("IFA_B200_NO_PP");
