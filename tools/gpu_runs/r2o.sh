@@ -1,0 +1,10 @@
+#!/usr/bin/env bash
+set -u
+OUT=gpurun_out/r2o; mkdir -p $OUT
+B="timeout 300 python bench.py --steps 10 --warmup 3 --no-extras"
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_dump.py tests/test_gpu_half.py tests/test_gpu_fp8.py tests/test_gpu_longseq.py -q -x --timeout 600 > $OUT/pytest.log 2>&1; echo "exit $?" >> $OUT/pytest.log
+$B > $OUT/c2.json 2>>$OUT/err.txt
+$B --workload c3 > $OUT/c3.json 2>>$OUT/err.txt
+$B --workload c5 --steps 3 > $OUT/c5.json 2>>$OUT/err.txt
+IFA_B200_LIB=build/pptrace/libifa_b200.so timeout 300 python tools/pp_trace.py > $OUT/pp_trace.txt 2>&1
+echo done > $OUT/DONE
