@@ -429,34 +429,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // Warp 1 issues group 0's MMAs, warp 2 group 1's, so neither group
             // waits on the other's progress.  Per block j: S(next) as soon as the
             // group has read S(j), then P.V(j) once it has published P(j).
-            if (lane == 0) {
+            // The whole warp runs the loop (warp-uniform descriptors live in
+            // uniform registers) and one elected lane issues each batch: with
+            // only lane 0 running it, every descriptor went through R2UR and an
+            // MMA took ~135 cycles to issue (tools/pp_trace.py), twice the
+            // tensor core's own 65-90 (tools/microbench/mma_issue.cu).
+            {
                 const int g = static_cast<int>(warp) - 1;
                 Ring<KST> kr;     // K stage of block j
                 Ring<VST> vr;     // V stage of block j
                 uint32_t t = 0;   // tiles of this group so far
                 uint32_t wi = 0;
                 const uint32_t d_s = tmem + 256 * g, d_o = d_s + 128;
+                // descriptor + (byte offset >> 4) addresses the same layout at an
+                // offset (shared memory < 256 KiB: no carry out of the 14-bit field)
+                const uint64_t q_desc = smem_desc(smem_u32(sm.q[g]), 16, kSbo, kLayout);
+                const uint64_t p_desc = smem_desc(smem_u32(sm.p[g]), 16, 1024, kLayoutSw128);
                 auto issue_s = [&](uint32_t ks, uint32_t kph) {
                     bar_wait(b_k_full + 8 * ks, kph);
                     tc_fence_after();
-                    const uint32_t q_base = smem_u32(sm.q[g]);
-                    const uint32_t k_base = smem_u32(sm.k[ks]);
+                    const uint64_t k_desc = smem_desc(smem_u32(sm.k[ks]), 16, kSbo, kLayout);
+                    if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < D / 32; ++kk) {
-                        const uint64_t adesc = smem_desc(q_base + kk * 32, 16, kSbo, kLayout);
-                        const uint64_t bdesc = smem_desc(k_base + kk * 32, 16, kSbo, kLayout);
-                        if constexpr (MODE == kModeFp8)
-                            mma_f8_ss(d_s, adesc, bdesc, kIdescS, kk > 0 ? 1u : 0u);
-                        else
-                            mma_i8_ss(d_s, adesc, bdesc, kIdescS, kk > 0 ? 1u : 0u);
+                        for (int kk = 0; kk < D / 32; ++kk) {
+                            if constexpr (MODE == kModeFp8)
+                                mma_f8_ss(d_s, q_desc + 2 * kk, k_desc + 2 * kk, kIdescS,
+                                          kk > 0 ? 1u : 0u);
+                            else
+                                mma_i8_ss(d_s, q_desc + 2 * kk, k_desc + 2 * kk, kIdescS,
+                                          kk > 0 ? 1u : 0u);
+                        }
+                        mma_commit_u32(b_s_full + 8 * g);
                     }
-                    mma_commit_u32(b_s_full + 8 * g);
+                    __syncwarp();
                 };
                 if (blockIdx.x < p.items) {
                     bar_wait(b_q_full, 0);
                     issue_s(0, 0);
                 }
-                const uint32_t p_base = smem_u32(sm.p[g]);
                 for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x, ++wi) {
                     const bool has_next_item = idx + static_cast<int32_t>(gridDim.x) < p.items;
                     const PWork w = pwork(idx, p, causal, J);
@@ -464,19 +474,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     for (int32_t j = 0; j < w.jt; ++j) {
                         if (j >= jg) {  // causal: a KV tile only the other group reads
                             bar_wait(b_k_full + 8 * kr.idx, kr.phase);
-                            bar_arrive(b_k_empty + 8 * kr.idx);
+                            if (elect_one()) bar_arrive(b_k_empty + 8 * kr.idx);
+                            __syncwarp();
                             bar_wait(b_v_full + 8 * vr.idx, vr.phase);
-                            bar_arrive(b_v_empty + 8 * vr.idx);
+                            if (elect_one()) bar_arrive(b_v_empty + 8 * vr.idx);
+                            __syncwarp();
                             kr.advance();
                             vr.advance();
                             continue;
                         }
                         const bool last = j == jg - 1;
-                        mma_commit_u32(b_k_empty + 8 * kr.idx);  // S(j) issued
-                        if (last) {
-                            mma_commit_u32(b_q_empty);  // every S of this item issued
-                            if (has_next_item) bar_wait(b_q_full, (wi + 1) & 1);
+                        if (elect_one()) {
+                            mma_commit_u32(b_k_empty + 8 * kr.idx);  // S(j) issued
+                            if (last) mma_commit_u32(b_q_empty);     // every S of this item issued
                         }
+                        __syncwarp();
+                        if (last && has_next_item) bar_wait(b_q_full, (wi + 1) & 1);
                         if (!last || has_next_item) {
                             // next S: tile j+1, or tile 0 of the next item (jt - j ring
                             // positions ahead)
@@ -485,27 +498,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             for (int32_t a = 0; a < ahead; ++a) nk.advance();
                             bar_wait(b_s_empty + 8 * g, t & 1);
                             issue_s(nk.idx, nk.phase);
-                            PP_TR(1, g, t, 0);
+                            if (lane == 0) PP_TR(1, g, t, 0);
                         }
                         bar_wait(b_v_full + 8 * vr.idx, vr.phase);
-                        const uint32_t v_base = smem_u32(sm.v[vr.idx]);
+                        const uint64_t v_desc =
+                            smem_desc(smem_u32(sm.v[vr.idx]), BN * 128, 1024, kLayoutSw128);
                         bar_wait(b_p_full + 8 * g, t & 1);
-                        PP_TR(1, g, t, 1);
+                        if (lane == 0) PP_TR(1, g, t, 1);
                         if (j == 0 && wi > 0) bar_wait(b_o_free + 8 * g, (wi - 1) & 1);
                         tc_fence_after();
+                        if (elect_one()) {
 #pragma unroll
-                        for (int kk = 0; kk < BN / 16; ++kk) {
-                            const uint64_t adesc = smem_desc(
-                                p_base + (kk >> 2) * (BM * 128) + (kk & 3) * 32, 16, 1024,
-                                kLayoutSw128);
-                            const uint64_t bdesc =
-                                smem_desc(v_base + kk * 16 * 128, BN * 128, 1024, kLayoutSw128);
-                            mma_f16_ss(d_o, adesc, bdesc, kIdescPV, (j == 0 && kk == 0) ? 0u : 1u);
+                            for (int kk = 0; kk < BN / 16; ++kk)
+                                mma_f16_ss(d_o, p_desc + (kk >> 2) * (BM * 128 / 16) + (kk & 3) * 2,
+                                           v_desc + kk * (16 * 128 / 16), kIdescPV,
+                                           (j == 0 && kk == 0) ? 0u : 1u);
+                            mma_commit_u32(b_p_empty + 8 * g);
+                            if (last) mma_commit_u32(b_o_full + 8 * g);
+                            mma_commit_u32(b_v_empty + 8 * vr.idx);
                         }
-                        mma_commit_u32(b_p_empty + 8 * g);
-                        PP_TR(1, g, t, 2);
-                        if (last) mma_commit_u32(b_o_full + 8 * g);
-                        mma_commit_u32(b_v_empty + 8 * vr.idx);
+                        __syncwarp();
+                        if (lane == 0) PP_TR(1, g, t, 2);
                         kr.advance();
                         vr.advance();
                         ++t;

@@ -22,11 +22,12 @@ constexpr int TILES = 32;  // 8 MMAs each
 __global__ void __launch_bounds__(640, 1) bench(long long* out, int variant, int busy, uint32_t rt_off) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ uint64_t bar;
+    __shared__ uint64_t cbar[8];
     __shared__ uint32_t tbase;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t(1023));
     for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(base)[i] = 0x3c003c00u;
-    if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); for (int i = 0; i < 8; ++i) mbar_init(&cbar[i], 1); fence_barrier_init(); }
     if (warp == 0) tmem_alloc<512>(&tbase);
     fence_proxy_async_shared();
     tc_fence_before(); __syncthreads(); tc_fence_after();
@@ -101,6 +102,31 @@ __global__ void __launch_bounds__(640, 1) bench(long long* out, int variant, int
                     mma_commit_u32(bb);
                 }
                 __syncwarp();
+            } else if (variant == 7 || variant == 8) {  // the mix + the kernel's commits per tile
+                constexpr uint32_t kIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+                if (lane == 0) {
+                    for (int t = 0; t < TILES; ++t) {
+                        const uint32_t so = 256 * (t & 1);
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const uint64_t ad = smem_desc(p_base + kk * 32, 16, 1024, kLayoutSw128);
+                            const uint64_t bd = smem_desc(v_base + kk * 32, 16, 1024, kLayoutSw128);
+                            mma_i8_ss(tm + so, ad, bd, kIdescI8, kk ? 1u : 0u);
+                        }
+                        mma_commit_u32(smem_u32(&cbar[0]));  // s_full
+                        if (variant == 8) mma_commit_u32(smem_u32(&cbar[1]));  // k_empty
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) {
+                            const uint64_t ad = smem_desc(p_base + (kk >> 2) * (128 * 128) + (kk & 3) * 32, 16, 1024, kLayoutSw128);
+                            const uint64_t bd = smem_desc(v_base + kk * 16 * 128, 128 * 128, 1024, kLayoutSw128);
+                            mma_f16_ss(tm + so + 128, ad, bd, kIdesc, 1u);
+                        }
+                        mma_commit_u32(smem_u32(&cbar[2]));  // p_empty
+                        if (variant == 8) { mma_commit_u32(smem_u32(&cbar[3])); mma_commit_u32(smem_u32(&cbar[4])); }  // v_empty, ...
+                    }
+                    mma_commit_u32(bb);
+                }
+                __syncwarp();
             } else if (variant == 3) {  // the kernel's form: runtime slot offsets, lane 0
                 if (lane == 0) {
                     for (int t = 0; t < TILES; ++t) {
@@ -147,10 +173,11 @@ int main() {
     long long* d; cudaMalloc(&d, 148 * 8);
     cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
     const char* names[] = {"lane 0 issues, descriptors per MMA", "whole warp + elect.sync per MMA", "lane 0, descriptors precomputed", "lane 0, runtime slot offsets (kernel form)",
-                           "mix: 4 i8 S + 8 f16 PV per tile, 1 group", "mix, two groups' TMEM alternating", "4 f16 + 8 f16 per tile (no kind switch)"};
+                           "mix: 4 i8 S + 8 f16 PV per tile, 1 group", "mix, two groups' TMEM alternating", "4 f16 + 8 f16 per tile (no kind switch)",
+                           "mix + 2 commits per tile", "mix + 5 commits per tile (the kernel's)"};
     const char* bn[] = {"quiet SMSP", "+4 FFMA warps on the SMSP", "+4 FFMA+MUFU warps"};
     for (int busy = 0; busy < 2; ++busy)
-        for (int v = 3; v < 7; ++v) {
+        for (int v : {5, 7, 8}) {
             bench<<<148, 640, 80 * 1024>>>(d, v, busy, 0);
             cudaError_t e = cudaDeviceSynchronize();
             long long h; cudaMemcpy(&h, d + 1, 8, cudaMemcpyDeviceToHost);
