@@ -795,7 +795,10 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
         }
       } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        // Warp-wide loop, one elected lane per MMA batch: the descriptors stay
+        // in uniform registers (with lane 0 alone every operand went through
+        // R2UR and an MMA took ~2x the tensor core's time to issue, attn_pp.cu).
+        {
             const uint32_t ones_base = smem_u32(sm.ones);
             Ring<STAGES> kv;
             uint32_t i = 0, pi = 0, bi = 0, wi = 0;
@@ -808,24 +811,26 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
                 bar_wait(b_v_full + 8 * st, ph);
                 if ((kind & K_PV_FIRST) && bi >= 1) bar_wait(b_pv_empty, (bi - 1) & 1);
                 tc_fence_after();
-                const uint32_t v_base = smem_u32(sm.v[st]);
+                const uint64_t v_desc = smem_desc(smem_u32(sm.v[st]), 16, kSbo, kLayout);
+                const uint64_t o_desc = smem_desc(ones_base, 16, 1024, kLayoutSw128);
                 const uint32_t p_col = T_P0 + 32 * (pidx & 1);
+                if (elect_one()) {
 #pragma unroll
-                for (int kk = 0; kk < BN / 32; ++kk) {
-                    // B = V tile, MN-major: 32 keys x D per step = 32 rows of D bytes.
-                    const uint64_t bdesc = smem_desc(v_base + kk * 32 * D, 16, kSbo, kLayout);
-                    const uint32_t acc = ((kind & K_PV_FIRST) && kk == 0) ? 0u : 1u;
-                    mma_i8_ts(tmem + T_PV, tmem + p_col + kk * 8, bdesc, kIdescPV, acc);
-                    // P . 1 (16 identical columns): the block's exact code row sum.
-                    const uint64_t odesc = smem_desc(ones_base + kk * 32, 16, 1024, kLayoutSw128);
-                    mma_i8_ts(tmem + T_RS, tmem + p_col + kk * 8, odesc, kIdescSum, acc);
+                    for (int kk = 0; kk < BN / 32; ++kk) {
+                        // B = V tile, MN-major: 32 keys x D per step = 32 rows of D bytes.
+                        const uint32_t acc = ((kind & K_PV_FIRST) && kk == 0) ? 0u : 1u;
+                        mma_i8_ts(tmem + T_PV, tmem + p_col + kk * 8, v_desc + kk * (32 * D / 16),
+                                  kIdescPV, acc);
+                        // P . 1 (16 identical columns): the block's exact code row sum.
+                        mma_i8_ts(tmem + T_RS, tmem + p_col + kk * 8, o_desc + kk * 2, kIdescSum,
+                                  acc);
+                    }
+                    mma_commit_u32(b_p_empty + 8 * (pidx & 1));
+                    mma_commit_u32(b_kv_empty + 8 * st);
+                    if (kind & K_END) mma_commit_u32(b_pv_full);
                 }
-                mma_commit_u32(b_p_empty + 8 * (pidx & 1));
-                mma_commit_u32(b_kv_empty + 8 * st);
-                if (kind & K_END) {
-                    mma_commit_u32(b_pv_full);
-                    ++bi;
-                }
+                __syncwarp();
+                if (kind & K_END) ++bi;
             };
             for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x, ++wi) {
                 const Work w = work_of(idx, p, causal);
@@ -841,15 +846,17 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
                     bar_wait(b_k_full + 8 * st, ph);
                     if (i > 0) bar_wait(b_s_empty, (i - 1) & 1);
                     tc_fence_after();
-                    const uint32_t k_base = smem_u32(sm.k[st]);
+                    const uint64_t q_desc = smem_desc(q_base, 16, kSbo, kLayout);
+                    const uint64_t k_desc = smem_desc(smem_u32(sm.k[st]), 16, kSbo, kLayout);
+                    if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < D / 32; ++kk) {
-                        const uint64_t adesc = smem_desc(q_base + kk * 32, 16, kSbo, kLayout);
-                        const uint64_t bdesc = smem_desc(k_base + kk * 32, 16, kSbo, kLayout);
-                        mma_i8_ss(tmem + T_S, adesc, bdesc, kIdescS, kk > 0 ? 1u : 0u);
+                        for (int kk = 0; kk < D / 32; ++kk)
+                            mma_i8_ss(tmem + T_S, q_desc + 2 * kk, k_desc + 2 * kk, kIdescS,
+                                      kk > 0 ? 1u : 0u);
+                        mma_commit_u32(b_s_full);
+                        if (!(it.kind & K_PV)) mma_commit_u32(b_kv_empty + 8 * st);
                     }
-                    mma_commit_u32(b_s_full);
-                    if (!(it.kind & K_PV)) mma_commit_u32(b_kv_empty + 8 * st);
+                    __syncwarp();
                     if (have_prev) issue_pv(prev_st, prev_ph, prev_kind, prev_pi);
                     if (it.kind & K_PV) {
                         have_prev = true;
@@ -864,7 +871,8 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
                     ++i;
                 }
                 // every S MMA reading this Q buffer has been issued
-                mma_commit_u32(b_q_empty + 8 * qb);
+                if (elect_one()) mma_commit_u32(b_q_empty + 8 * qb);
+                __syncwarp();
             }
             if (have_prev) issue_pv(prev_st, prev_ph, prev_kind, prev_pi);
         }
