@@ -123,6 +123,7 @@ struct Params {
     int32_t n, d;
     int32_t n_pad;    // rows per slice of the fp16 V buffer (n rounded up to 128)
     int32_t o_pitch;  // floats per O row (even: the epilogue stores 8-byte pairs)
+    int32_t o_tma;    // 1: the epilogue stages O in shared memory and TMA-stores it (tm_o)
     float sk_mul;  // log2(e) [* 1/sqrt(d)]: scores are kept in the log2 domain
     uint32_t flags;
     int32_t pairs, slices, items;
@@ -301,7 +302,8 @@ template <int D, bool CAUSAL, int MODE, bool RAGGED, bool STREAMED = false, bool
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     int_flash_pp_kernel(const __grid_constant__ CUtensorMap tm_q,
                         const __grid_constant__ CUtensorMap tm_k,
-                        const __grid_constant__ CUtensorMap tm_v, const Params p) {
+                        const __grid_constant__ CUtensorMap tm_v,
+                        const __grid_constant__ CUtensorMap tm_o, const Params p) {
     constexpr uint32_t kLayout = D == 128 ? kLayoutSw128 : kLayoutSw64;
     constexpr uint32_t kSbo = 8 * D;
     constexpr uint32_t kIdescS = MODE == kModeFp8
@@ -885,8 +887,68 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     // V = decode / sV; an all-zero V slice (sV = 0) gives O = 0
                     f[r] = p.sv[slice] == 0.0f ? 0.0f : __fdiv_rn(__fdiv_rn(1.0f, lt), p.sv[slice]);
             }
+            const bool tre = (mw & 7) == 0 && lane == 0;
+            if (tre) PP_TR(1, g, tc - 1, 5);
             bar_wait(bo_full, wi & 1);
+            if (tre) PP_TR(1, g, tc - 1, 6);
             tc_fence_after();
+            if (p.o_tma) {
+                // Stage O through the group's (now idle) P buffer, 64 columns
+                // at a time as two 128 x 32 f32 SW128 boxes, and TMA-store it:
+                // full-line writes by the TMA engine instead of 8-byte stores
+                // scattered over 8 rows per instruction (~6,000 cycles per item
+                // epilogue, tools/pp_trace.py).  Rows past n are clipped by TMA.
+                constexpr float os = MODE == kModeCodes ? 16777216.0f : 1.0f;
+                const uint32_t stage = smem_u32(sm.p[g]);
+                const bool issuer = (mw & 7) == 0 && lane == 0;
+#pragma unroll
+                for (int hh = 0; hh < D / 64; ++hh) {
+                    if (hh > 0) {  // the previous half's boxes have been read
+                        if (issuer) tma_store_wait_read();
+                        named_bar_sync(1 + g, 256);
+                    }
+#pragma unroll
+                    for (int cc = 0; cc < 2; ++cc) {
+                        const int c = 2 * hh + cc;
+                        uint32_t o[16];
+                        ld16x256_x4(t_o + 32 * c, o);
+                        tmem_wait_ld();
+                        if (c == D / 32 - 1) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) bar_arrive(bo_free);
+                        }
+                        const uint32_t box = stage + cc * (BM * 128);
+#pragma unroll
+                        for (int r = 0; r < 2; ++r) {
+                            const uint32_t row = static_cast<uint32_t>(row0 + 8 * r);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const uint32_t q16 = (2 * k + (t0 >> 1)) ^ (row & 7);
+                                const float vx = __uint_as_float(o[4 * k + 2 * r]) * os * f[r];
+                                const float vy = __uint_as_float(o[4 * k + 2 * r + 1]) * os * f[r];
+                                asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(
+                                                 box + row * 128 + q16 * 16 + (t0 & 1) * 8),
+                                             "f"(vx), "f"(vy)
+                                             : "memory");
+                            }
+                        }
+                    }
+                    fence_proxy_async_shared();
+                    named_bar_sync(1 + g, 256);
+                    if (issuer) {
+                        tma_store_3d(&tm_o, reinterpret_cast<const void*>(sm.p[g]), 64 * hh, q0, slice);
+                        tma_store_3d(&tm_o, reinterpret_cast<const uint8_t*>(sm.p[g]) + BM * 128,
+                                     64 * hh + 32, q0, slice);
+                        tma_store_commit();
+                    }
+                }
+                // the next item's P stores reuse the buffer
+                if (issuer) tma_store_wait_read();
+                named_bar_sync(1 + g, 256);
+                if (tre) PP_TR(1, g, tc - 1, 7);
+                continue;
+            }
 #pragma unroll
             for (int c = 0; c < D / 32; ++c) {
                 uint32_t o[16];
@@ -918,6 +980,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     }
 
+    if (p.o_tma) tma_store_wait_all();  // the last item's O stores
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -1011,14 +1074,38 @@ static bool make_map_v16(CUtensorMap* map, const __half* base, int64_t slices, i
            CUDA_SUCCESS;
 }
 
+// f32 O [slices][n][o_pitch] (d valid columns), box {32 cols, 128 rows, 1}, SW128
+static bool make_map_o(CUtensorMap* map, const float* base, int64_t slices, int64_t n, int64_t d,
+                       int64_t o_pitch) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc || (o_pitch * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0)
+        return false;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(n),
+                                static_cast<cuuint64_t>(slices)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(o_pitch) * 4,
+                                   static_cast<cuuint64_t>(o_pitch) * 4 * n};
+    const cuuint32_t box[3] = {32u, 128u, 1u};
+    const cuuint32_t estr[3] = {1u, 1u, 1u};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
+               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int D, int MODE>
-static cudaError_t run(const void* q, const void* k, const __half* v16, const Params& p,
+static cudaError_t run(const void* q, const void* k, const __half* v16, const Params& p_in,
                        int64_t pitch, bool causal, cudaStream_t stream) {
-    CUtensorMap tq, tk, tv;
-    if (!make_map_codes(&tq, static_cast<const int8_t*>(q), p.slices, p.n, pitch, D) ||
-        !make_map_codes(&tk, static_cast<const int8_t*>(k), p.slices, p.n, pitch, D) ||
-        !make_map_v16(&tv, v16, p.slices, p.n_pad, D))
+    CUtensorMap tq, tk, tv, to;
+    if (!make_map_codes(&tq, static_cast<const int8_t*>(q), p_in.slices, p_in.n, pitch, D) ||
+        !make_map_codes(&tk, static_cast<const int8_t*>(k), p_in.slices, p_in.n, pitch, D) ||
+        !make_map_v16(&tv, v16, p_in.slices, p_in.n_pad, D))
         return cudaErrorInvalidValue;
+    Params p = p_in;
+    const char* no_tma = std::getenv("IFA_B200_NO_OTMA");
+    p.o_tma = (!(no_tma && no_tma[0] == '1') && p.s_dump == nullptr && p.p_dump == nullptr &&
+               make_map_o(&to, p.o, p.slices, p.n, p.d, p.o_pitch))
+                  ? 1
+                  : 0;
+    if (!p.o_tma) to = tq;  // unused
     const size_t smem = sizeof(Smem<D>) + 1024;
     cudaError_t e = smem_attr_once<int_flash_pp_kernel<D, false, MODE, false>>(smem);
     if (e == cudaSuccess && MODE == kModeCodes) {
@@ -1037,12 +1124,12 @@ static cudaError_t run(const void* q, const void* k, const __half* v16, const Pa
                 e = smem_attr_once<int_flash_pp_kernel<D, true, MODE, true, false, true>>(smem);
                 if (e == cudaSuccess)
                     int_flash_pp_kernel<D, true, MODE, true, false, true>
-                        <<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+                        <<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, to, p);
             } else {
                 e = smem_attr_once<int_flash_pp_kernel<D, false, MODE, true, false, true>>(smem);
                 if (e == cudaSuccess)
                     int_flash_pp_kernel<D, false, MODE, true, false, true>
-                        <<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+                        <<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, to, p);
             }
             if (e != cudaSuccess) return e;
         } else if (p.ready != nullptr) {  // streamed step: non-causal, n % 128 == 0 only
@@ -1050,17 +1137,17 @@ static cudaError_t run(const void* q, const void* k, const __half* v16, const Pa
             e = smem_attr_once<int_flash_pp_kernel<D, false, MODE, false, true>>(smem);
             if (e != cudaSuccess) return e;
             int_flash_pp_kernel<D, false, MODE, false, true><<<grid, NUM_THREADS, smem, stream>>>(
-                tq, tk, tv, p);
+                tq, tk, tv, to, p);
         } else if (causal && ragged)
-            int_flash_pp_kernel<D, true, MODE, true><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+            int_flash_pp_kernel<D, true, MODE, true><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, to, p);
         else if (causal)
-            int_flash_pp_kernel<D, true, MODE, false><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+            int_flash_pp_kernel<D, true, MODE, false><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, to, p);
         else if (ragged)
-            int_flash_pp_kernel<D, false, MODE, true><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+            int_flash_pp_kernel<D, false, MODE, true><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, to, p);
         else
-            int_flash_pp_kernel<D, false, MODE, false><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+            int_flash_pp_kernel<D, false, MODE, false><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, to, p);
     } else {  // half-INT8 / FP8: non-causal, n % 128 == 0 (float_weights_pp_eligible)
-        int_flash_pp_kernel<D, false, MODE, false><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, p);
+        int_flash_pp_kernel<D, false, MODE, false><<<grid, NUM_THREADS, smem, stream>>>(tq, tk, tv, to, p);
     }
     return cudaGetLastError();
 }
@@ -1088,6 +1175,7 @@ static Params make_params(const float* sq, const float* sk, const float* sv, flo
     p.max_ctas = 0;
     p.s_dump = nullptr;
     p.p_dump = nullptr;
+    p.o_tma = 0;
     return p;
 }
 

@@ -38,7 +38,7 @@ def main():
     t0 = t[t > 0].min()
     rel = np.where(t > 0, t - t0, -1)
     print("tile | g0: W S L M F C P | mma0: Sn Pok PV | g1: W S L M F C P | mma1: Sn Pok PV")
-    for tile in range(40, 60):
+    for tile in [int(x) for x in os.environ.get("PP_TRACE_TILES", "28,29,30,31,32,33,34,35,60,61,62,63,64,65").split(",")]:
         cells = []
         for gr in range(2):
             m = rel[0, gr, tile]
@@ -46,6 +46,13 @@ def main():
             mm = rel[1, gr, tile]
             cells.append(" ".join(f"{x:8d}" for x in mm[:3]))
         print(f"{tile:4d} | " + " | ".join(cells))
+    for gr in range(2):
+        mm = rel[1, gr]
+        ends = [i for i in range(1024) if mm[i, 5] > 0]
+        for i in ends[:4]:
+            nxt = rel[0, gr, i + 1, 7] if i + 1 < 1024 else -1
+            print(f"group {gr} item end at tile {i}: P published {rel[0, gr, i, 5]}, epilogue start "
+                  f"{mm[i, 5]}, o_full {mm[i, 6]}, epilogue done {mm[i, 7]}, next tile wait {nxt}")
     for gr in range(2):
         m = t[0, gr]
         ok = np.all(m[:, [7, 0, 1, 2, 3, 4, 5]] > 0, axis=1)
