@@ -75,8 +75,10 @@ constexpr float kLog2e = 1.4426950408889634f;
 // unit keeps up: C2 0.982 ms at 16 vs 0.989 at 15 and 0.985 at 7 (with the
 // groups de-phased; 1.029 at 15 vs 1.034 at 16 before).
 constexpr int kPolyMask = IFA_PP_POLY_MASK;
+// group 1's start delay (ns): 1000 helped before the warp-wide MMA issue
+// (0.994 -> 0.983 ms); since then 0 is best (0.921 vs 0.928 ms at 1000)
 #ifndef IFA_PP_G1_DELAY_NS
-#define IFA_PP_G1_DELAY_NS 1000
+#define IFA_PP_G1_DELAY_NS 0
 #endif
 // Cold-code skipping (kModeCodes): a code round(127 * 2^t') is 0 whenever
 // t = t' + log2(127) < -1, i.e. when the score is more than ln(254) below the
