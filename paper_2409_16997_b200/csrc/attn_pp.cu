@@ -100,6 +100,11 @@ constexpr int kPolyMask = IFA_PP_POLY_MASK;
 #ifndef IFA_PP_SPARSE_HOT
 #define IFA_PP_SPARSE_HOT 16
 #endif
+// float(S) by integer magic add + packed subtract instead of I2F
+#ifndef IFA_PP_MAGIC_CVT
+#define IFA_PP_MAGIC_CVT 0
+#endif
+constexpr bool kMagicCvt = IFA_PP_MAGIC_CVT != 0;
 #ifndef IFA_PP_EARLY_P
 #define IFA_PP_EARLY_P 1
 #endif
@@ -493,17 +498,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             if (last) mma_commit_u32(b_q_empty);     // every S of this item issued
                         }
                         __syncwarp();
-                        if (last && has_next_item) bar_wait(b_q_full, (wi + 1) & 1);
-                        if (!last || has_next_item) {
-                            // next S: tile j+1, or tile 0 of the next item (jt - j ring
-                            // positions ahead)
+                        // next S: tile j+1 now; tile 0 of the next item (jt - j ring
+                        // positions ahead) only after this item's last P.V, which the
+                        // epilogue waits for -- not behind the next item's Q load
+                        auto next_s = [&]() {
                             Ring<KST> nk = kr;
                             const int32_t ahead = last ? w.jt - j : 1;
                             for (int32_t a = 0; a < ahead; ++a) nk.advance();
                             bar_wait(b_s_empty + 8 * g, t & 1);
                             issue_s(nk.idx, nk.phase);
                             if (lane == 0) PP_TR(1, g, t, 0);
-                        }
+                        };
+                        if (!last) next_s();
                         bar_wait(b_v_full + 8 * vr.idx, vr.phase);
                         const uint64_t v_desc =
                             smem_desc(smem_u32(sm.v[vr.idx]), BN * 128, 1024, kLayoutSw128);
@@ -523,6 +529,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         }
                         __syncwarp();
                         if (lane == 0) PP_TR(1, g, t, 2);
+                        if (last && has_next_item) {
+                            bar_wait(b_q_full, (wi + 1) & 1);
+                            next_s();
+                        }
                         kr.advance();
                         vr.advance();
                         ++t;
@@ -634,6 +644,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     if constexpr (MODE == kModeFp8) {
                         fa = make_float2(__uint_as_float(sr[4 * k]), __uint_as_float(sr[4 * k + 1]));
                         fb = make_float2(__uint_as_float(sr[4 * k + 2]), __uint_as_float(sr[4 * k + 3]));
+                    } else if constexpr (kMagicCvt) {
+                        // |S| <= 127^2 * 128 < 2^22: the bits of S + 0x4B400000 are
+                        // the float 1.5 * 2^23 + S, so one exact packed subtract
+                        // leaves float(S) (integer adds on the ALU instead of the
+                        // quarter-rate I2F pipe)
+                        fa = fsub2(make_float2(__uint_as_float(sr[4 * k] + 0x4B400000u),
+                                               __uint_as_float(sr[4 * k + 1] + 0x4B400000u)),
+                                   f2(kMagic));
+                        fb = fsub2(make_float2(__uint_as_float(sr[4 * k + 2] + 0x4B400000u),
+                                               __uint_as_float(sr[4 * k + 3] + 0x4B400000u)),
+                                   f2(kMagic));
                     } else {
                         fa = make_float2(__int2float_rn(static_cast<int32_t>(sr[4 * k])),
                                          __int2float_rn(static_cast<int32_t>(sr[4 * k + 1])));
