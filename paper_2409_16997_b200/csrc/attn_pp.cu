@@ -59,10 +59,17 @@ constexpr int VST = IFA_PP_VST;  // fp16 V tiles in flight
 constexpr int CTRL_WARPS = 4;
 constexpr int GROUP_WARPS = 8;
 constexpr int NUM_THREADS = 32 * (CTRL_WARPS + 2 * GROUP_WARPS);
-constexpr uint32_t kRegsControl = 32;
+#ifndef IFA_PP_REGS_CONTROL
+#define IFA_PP_REGS_CONTROL 32
+#endif
+constexpr uint32_t kRegsControl = IFA_PP_REGS_CONTROL;
 // setmaxnreg moves registers inside the CTA pool allocated at launch (640 x 96
 // = 61440): 4*32*32 + 16*32*112 = 61440.
-constexpr uint32_t kRegsMath = 112;
+#ifndef IFA_PP_REGS_MATH
+#define IFA_PP_REGS_MATH 112
+#endif
+constexpr uint32_t kRegsMath = IFA_PP_REGS_MATH;
+static_assert(4 * kRegsControl + 16 * kRegsMath <= 640 * 96 / 32, "setmaxnreg pool");
 constexpr uint32_t TMEM_COLS = 512;
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
 constexpr float kLog2_127 = 6.9886846867721655f;

@@ -312,13 +312,18 @@ constexpr int kSliceCluster = 8;
 
 // Four packed int8 codes -> four fp16 (exact), for the two-Q-tile attention
 // kernel's P.V operand.
+// Without the quarter-rate I2F.F16 conversions (the V kernel's XU pipe ran at
+// 85%): u = c + 128 in [1, 255] (XOR 0x80 per byte) placed under the fp16
+// exponent byte 0x66 is the half 1536 + u exactly (ulp 1 in [1024, 2048)), and
+// one packed subtract of 1664 leaves c exactly.
 __device__ __forceinline__ uint2 codes4_to_f16(uint32_t w) {
-    const __half2 lo = __halves2half2(__int2half_rn(static_cast<int8_t>(w & 0xff)),
-                                      __int2half_rn(static_cast<int8_t>((w >> 8) & 0xff)));
-    const __half2 hi = __halves2half2(__int2half_rn(static_cast<int8_t>((w >> 16) & 0xff)),
-                                      __int2half_rn(static_cast<int8_t>(w >> 24)));
-    return make_uint2(*reinterpret_cast<const uint32_t*>(&lo),
-                      *reinterpret_cast<const uint32_t*>(&hi));
+    const uint32_t u = w ^ 0x80808080u;
+    const uint32_t lo = __byte_perm(u, 0x66666666u, 0x4140);  // halves 1536 + u0, 1536 + u1
+    const uint32_t hi = __byte_perm(u, 0x66666666u, 0x4342);
+    const __half2 off = __float2half2_rn(1664.0f);
+    const __half2 l = __hsub2(*reinterpret_cast<const __half2*>(&lo), off);
+    const __half2 h = __hsub2(*reinterpret_cast<const __half2*>(&hi), off);
+    return make_uint2(*reinterpret_cast<const uint32_t*>(&l), *reinterpret_cast<const uint32_t*>(&h));
 }
 
 // F16: also write the codes as fp16 (codes16, same layout).
