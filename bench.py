@@ -761,6 +761,41 @@ def verify_ranks(torch, dist, plan, q, k, v, slices, N, d, bc, causal, fast, wor
     jobs = [(r, i) for r in range(world) for i in range(len(picks))]
     with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
         per_rank = list(ex.map(check, jobs))
+    # north_star "int32 S tiles bit-exact": one slice through the dump
+    # instantiation of the same kernel (ifa_int_flash_fwd_dump) -- S read back
+    # from the kind::i8 TMEM accumulator vs the oracle's int_gemm_nt
+    # (gemm.cpp:32-46), and the P codes vs the oracle's (the flip rate).
+    # Bounded to N <= 4096 (the oracle's GEMM is the cost).
+    s_check = None
+    if fast and N <= 4096 and bc == 128:
+        try:
+            import paper_2409_16997_b200 as ifa
+            inputs = ifa.QuantizedAttentionInputs(
+                ifa.QuantizedRows(plan.qc[:1], plan.sq[:1]),
+                ifa.QuantizedRows(plan.kc[:1], plan.sk[:1]),
+                ifa.QuantizedTensor(plan.vc[:1], plan.sv[:1]))
+            _, s_dev, p_dev = ifa.int_flash_attention_dump(
+                inputs, ifa.AttentionConfig(ifa.BlockSpec(128, 128), causal=causal))
+            q8 = plan.qc[0].cpu().numpy()
+            k8 = plan.kc[0].cpu().numpy()
+            v8 = plan.vc[0].cpu().numpy()
+            s_got = s_dev[0].cpu().numpy()
+            s_want = o.int_gemm_nt(q8, k8)
+            mask = np.ones_like(s_got, dtype=bool)
+            if causal:
+                rows = np.arange(N)[:, None] // 128
+                mask = (np.arange(N)[None, :] // 128) <= rows
+            _, p_want = o.int_flash_pcodes(q8, plan.sq[0].cpu().numpy(), k8,
+                                           plan.sk[0].cpu().numpy(), v8,
+                                           float(plan.sv[0].item()), 128, 128, flags=flags)
+            dp = np.where(mask, p_dev[0].cpu().numpy().astype(np.int32) - p_want, 0)
+            s_check = {"slice": 0, "s_tiles_bitwise_equal": bool(
+                np.array_equal(np.where(mask, s_got, 0), np.where(mask, s_want, 0))),
+                       "p_code_flips": int(np.count_nonzero(dp)),
+                       "p_codes_compared": int(mask.sum()),
+                       "p_code_max_abs_diff": int(np.abs(dp).max(initial=0))}
+        except Exception as e:  # pragma: no cover
+            s_check = {"error": str(e)[:200]}
     key = "within_tolerance" if fast else "bitwise_equal"
     out["parity"] = {
         "against": "oracle restatement (pinned bitwise to the reference, tests/test_oracle.py)"
@@ -769,6 +804,7 @@ def verify_ranks(torch, dist, plan, q, k, v, slices, N, d, bc, causal, fast, wor
         "bar": f"MRE <= {FAST_MRE} and max|dO| <= 2/127 max|V| sV" if fast else "bitwise",
         "per_rank": per_rank,
         "all_ok": all(p[key] for p in per_rank),
+        "s_tiles": s_check,
     }
     return out
 
