@@ -96,8 +96,10 @@ int ifa_quantize_per_tensor(const float* x, int64_t slices, int64_t rows, int64_
  *   audit: optional device ifa_pcode_audit.
  * sv values must be finite and >= 0 (validated by the host shims; the
  * reference rejects them in QuantizedAttentionInputs::validate).
- * Supported on the GPU: 1 <= d <= 128, n >= 1, bc >= 1.  d > 128 returns
- * IFA_ENOTSUP. */
+ * Supported on the GPU: 1 <= d <= 133144 (the reference's int32 depth limit,
+ * gemm.hpp:22), n >= 1, bc >= 1.  d > 128 runs the general kernel with S
+ * accumulated over 128-column depth chunks and one launch per 128 columns of
+ * O (attn.cu launch_wide). */
 int ifa_int_flash_fwd(const int8_t* q, const float* sq, const int8_t* k, const float* sk,
                       const int8_t* v, const float* sv, float* o, int64_t slices, int64_t n,
                       int64_t d, int64_t br, int64_t bc, uint32_t flags,

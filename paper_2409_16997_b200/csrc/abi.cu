@@ -89,9 +89,6 @@ int validate_fwd(int64_t slices, int64_t n, int64_t d, int64_t br, int64_t bc, u
                                        " exceeds 133144; int32 accumulation could overflow");
     if (flags & ~(IFA_FLAG_SQRT_D | IFA_FLAG_CAUSAL | IFA_FLAG_FAST))
         return fail(IFA_EINVAL, "int_flash_attention: unknown flag bits");
-    if (d > 128)
-        return fail(IFA_ENOTSUP, "int_flash_attention: head dim " + std::to_string(d) +
-                                     " > 128 is not supported by the sm_100a kernel");
     return IFA_OK;
 }
 
@@ -219,6 +216,9 @@ int ifa_int_flash_fwd_dump(const int8_t* q, const float* sq, const int8_t* k, co
     if (slices == 0) return IFA_OK;
     if (!(flags & IFA_FLAG_FAST))
         return fail(IFA_EINVAL, "int_flash_attention dump: needs IFA_FLAG_FAST");
+    if (d > 128)
+        return fail(IFA_ENOTSUP, "int_flash_attention dump: head dim " + std::to_string(d) +
+                                     " > 128 (the dump kernel holds one 128-column Q tile)");
     if (!(bc == 128 || (bc >= n && n <= 128)))
         return fail(IFA_ENOTSUP, "int_flash_attention dump: the tolerance kernel's KV block is "
                                  "128 keys (Bc = 128, or Bc >= n <= 128)");

@@ -203,6 +203,7 @@ struct alignas(1024) Smem {
     float bounds[128];         // B[k]: exact code decision boundaries (code_bounds.h)
     uint64_t q_full[2], q_empty[2];
     uint64_t k_full[STAGES], v_full[STAGES], kv_empty[STAGES];
+    uint64_t c_full[3], c_empty[3];  // head dims > 128: the (Q, K) depth-chunk ring
     uint64_t s_full, s_empty;
     uint64_t p_full[2], p_empty[2];
     uint64_t pv_full, pv_empty;
@@ -224,6 +225,13 @@ struct Params {
     int32_t q_tiles;
     int32_t slices;
     int32_t items;  // q_tiles * slices
+    // head dims > 128 (launch_wide): S accumulates over `wide_chunks` 128-column
+    // depth chunks of Q and K streamed through a 3-stage ring in the (then
+    // unused) Q and K buffers; this launch writes O columns [0, o_cols) of
+    // rows o_pitch floats apart (the V map and p.o start at the chunk's column)
+    int32_t wide_chunks = 0;
+    int32_t o_cols = 0;
+    int64_t o_pitch = 0;
     float bounds[128];
 };
 
@@ -694,6 +702,11 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
     const uint32_t b_s_full = smem_u32(&sm.s_full), b_s_empty = smem_u32(&sm.s_empty);
     const uint32_t b_p_full = smem_u32(&sm.p_full[0]), b_p_empty = smem_u32(&sm.p_empty[0]);
     const uint32_t b_pv_full = smem_u32(&sm.pv_full), b_pv_empty = smem_u32(&sm.pv_empty);
+    const uint32_t b_c_full = smem_u32(&sm.c_full[0]), b_c_empty = smem_u32(&sm.c_empty[0]);
+    // depth-chunk stage cs: (Q, K) in (k[0], k[1]), (k[2], k[3]), (q[0], q[1])
+    const bool wide = GENERIC && !QUAD && p.wide_chunks > 0;  // launch_wide uses GENERIC
+    auto chunk_q = [&](uint32_t cs) -> uint8_t* { return cs < 2 ? sm.k[2 * cs] : sm.q[0]; };
+    auto chunk_k = [&](uint32_t cs) -> uint8_t* { return cs < 2 ? sm.k[2 * cs + 1] : sm.q[1]; };
 
     if (threadIdx.x == 0) {
         if (smem_u32(smem_raw) & 1023) __trap();  // SWIZZLE_128B tiles need 1 KiB alignment
@@ -707,6 +720,10 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
             mbar_init(&sm.k_full[i], 32);
             mbar_init(&sm.v_full[i], 1);
             mbar_init(&sm.kv_empty[i], 1 + kMathWarps);
+        }
+        for (int i = 0; i < 3; ++i) {
+            mbar_init(&sm.c_full[i], 1);
+            mbar_init(&sm.c_empty[i], 1);
         }
         mbar_init(&sm.s_full, 1);
         mbar_init(&sm.s_empty, kMathWarps);
@@ -740,11 +757,11 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
             tma_prefetch_desc(&tm_v);
         }
         Ring<STAGES> kv;
-        uint32_t i = 0, wi = 0;
+        uint32_t i = 0, wi = 0, ci = 0;
         for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x, ++wi) {
             const Work w = work_of(idx, p, causal);
             const uint32_t qb = wi & 1;
-            if (lane == 0) {
+            if (lane == 0 && !wide) {
                 if (wi >= 2) bar_wait(b_q_empty + 8 * qb, ((wi >> 1) - 1) & 1);
                 mbar_arrive_expect_tx(&sm.q_full[qb], BM * D);
                 tma_load_3d(sm.q[qb], &tm_q, &sm.q_full[qb], 0, w.q0, w.slice, pol_stream);
@@ -773,8 +790,21 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
                 }
                 reinterpret_cast<float4*>(sm.sk[st])[lane] = kv4;
                 if (lane == 0) {
-                    mbar_arrive_expect_tx(&sm.k_full[st], kTileBytes);
-                    tma_load_3d(sm.k[st], &tm_k, &sm.k_full[st], 0, it.key0, w.slice, pol_keep);
+                    if (wide) {
+                        bar_arrive(b_k_full + 8 * st);  // the K scales only
+                        for (int32_t c = 0; c < p.wide_chunks; ++c, ++ci) {
+                            const uint32_t cs = ci % 3;
+                            if (ci >= 3) bar_wait(b_c_empty + 8 * cs, ((ci / 3) - 1) & 1);
+                            mbar_arrive_expect_tx(&sm.c_full[cs], 2 * kTileBytes);
+                            tma_load_3d(chunk_q(cs), &tm_q, &sm.c_full[cs], 128 * c, w.q0, w.slice,
+                                        pol_keep);
+                            tma_load_3d(chunk_k(cs), &tm_k, &sm.c_full[cs], 128 * c, it.key0,
+                                        w.slice, pol_keep);
+                        }
+                    } else {
+                        mbar_arrive_expect_tx(&sm.k_full[st], kTileBytes);
+                        tma_load_3d(sm.k[st], &tm_k, &sm.k_full[st], 0, it.key0, w.slice, pol_keep);
+                    }
                     if (it.kind & K_PV) {
                         mbar_arrive_expect_tx(&sm.v_full[st], kTileBytes);
                         if constexpr (QUAD)
@@ -801,7 +831,7 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
         {
             const uint32_t ones_base = smem_u32(sm.ones);
             Ring<STAGES> kv;
-            uint32_t i = 0, pi = 0, bi = 0, wi = 0;
+            uint32_t i = 0, pi = 0, bi = 0, wi = 0, ci = 0;
             bool have_prev = false;
             uint32_t prev_st = 0, prev_ph = 0, prev_kind = 0, prev_pi = 0;
             // P.V of a finished softmax item; issued after the next S so the
@@ -835,7 +865,7 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
             for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x, ++wi) {
                 const Work w = work_of(idx, p, causal);
                 const uint32_t qb = wi & 1;
-                bar_wait(b_q_full + 8 * qb, (wi >> 1) & 1);
+                if (!wide) bar_wait(b_q_full + 8 * qb, (wi >> 1) & 1);
                 tc_fence_after();
                 const uint32_t q_base = smem_u32(sm.q[qb]);
                 auto gen = make_gen<GENERIC>(n, p.bc, w.kv_limit);
@@ -846,6 +876,29 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
                     bar_wait(b_k_full + 8 * st, ph);
                     if (i > 0) bar_wait(b_s_empty, (i - 1) & 1);
                     tc_fence_after();
+                    if (wide) {
+                        // S = sum over the depth chunks (exact int32 accumulation)
+                        for (int32_t c = 0; c < p.wide_chunks; ++c, ++ci) {
+                            const uint32_t cs = ci % 3;
+                            bar_wait(b_c_full + 8 * cs, (ci / 3) & 1);
+                            tc_fence_after();
+                            const uint64_t qc = smem_desc(smem_u32(chunk_q(cs)), 16, kSbo, kLayout);
+                            const uint64_t kc = smem_desc(smem_u32(chunk_k(cs)), 16, kSbo, kLayout);
+                            if (elect_one()) {
+#pragma unroll
+                                for (int kk = 0; kk < D / 32; ++kk)
+                                    mma_i8_ss(tmem + T_S, qc + 2 * kk, kc + 2 * kk, kIdescS,
+                                              (c > 0 || kk > 0) ? 1u : 0u);
+                                mma_commit_u32(b_c_empty + 8 * cs);
+                            }
+                            __syncwarp();
+                        }
+                        if (elect_one()) {
+                            mma_commit_u32(b_s_full);
+                            if (!(it.kind & K_PV)) mma_commit_u32(b_kv_empty + 8 * st);
+                        }
+                        __syncwarp();
+                    } else {
                     const uint64_t q_desc = smem_desc(q_base, 16, kSbo, kLayout);
                     const uint64_t k_desc = smem_desc(smem_u32(sm.k[st]), 16, kSbo, kLayout);
                     if (elect_one()) {
@@ -857,6 +910,7 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
                         if (!(it.kind & K_PV)) mma_commit_u32(b_kv_empty + 8 * st);
                     }
                     __syncwarp();
+                    }
                     if (have_prev) issue_pv(prev_st, prev_ph, prev_kind, prev_pi);
                     if (it.kind & K_PV) {
                         have_prev = true;
@@ -871,7 +925,7 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
                     ++i;
                 }
                 // every S MMA reading this Q buffer has been issued
-                if (elect_one()) mma_commit_u32(b_q_empty + 8 * qb);
+                if (!wide && elect_one()) mma_commit_u32(b_q_empty + 8 * qb);
                 __syncwarp();
             }
             if (have_prev) issue_pv(prev_st, prev_ph, prev_kind, prev_pi);
@@ -1141,10 +1195,10 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
             }
 
             // epilogue: O = (acc / l) * sV (attention.cpp:335-342)
-            if (row_ok && c_base < p.d) {
+            if (row_ok && c_base < p.o_cols) {
                 const float sv = p.sv[w.slice];
-                const int32_t d = p.d;
-                float* orow = p.o + (static_cast<int64_t>(w.slice) * n + grow) * d + c_base;
+                const int32_t d = p.o_cols;
+                float* orow = p.o + (static_cast<int64_t>(w.slice) * n + grow) * p.o_pitch + c_base;
                 float out[NCOL];
                 if constexpr (FAST) {
                     const float f = __fdiv_rn(sv, l);
@@ -1154,7 +1208,7 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
 #pragma unroll
                     for (int c = 0; c < NCOL; ++c) out[c] = __fmul_rn(__fdiv_rn(acc[c], l), sv);
                 }
-                if (d % 4 == 0 && c_base + NCOL <= d) {
+                if (p.o_pitch % 4 == 0 && c_base + NCOL <= d) {
 #pragma unroll
                     for (int c = 0; c < NCOL; c += 4)
                         __stcs(reinterpret_cast<float4*>(orow + c),
@@ -1223,11 +1277,12 @@ static PFN_encodeTiled get_encode() {
 }
 
 // [slices][n][pitch] int8 codes, box = (D, 128 rows, 1 slice)
+// (cols = the row extent TMA may read, default the pitch; columns past it load as 0)
 static bool make_map(CUtensorMap* map, const int8_t* base, int64_t slices, int64_t n,
-                     int64_t pitch, int D) {
+                     int64_t pitch, int D, int64_t cols = 0) {
     PFN_encodeTiled enc = get_encode();
     if (!enc) return false;
-    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(pitch), static_cast<cuuint64_t>(n),
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols > 0 ? cols : pitch), static_cast<cuuint64_t>(n),
                                 static_cast<cuuint64_t>(slices)};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(pitch),
                                    static_cast<cuuint64_t>(pitch * n)};
@@ -1309,6 +1364,8 @@ static cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
     p.q_tiles = static_cast<int32_t>((a.n + BM - 1) / BM);
     p.slices = static_cast<int32_t>(a.slices);
     p.items = p.q_tiles * p.slices;
+    p.o_cols = p.d;
+    p.o_pitch = a.d;
     const float* bounds = code_bounds();
     for (int k = 0; k < 128; ++k) p.bounds[k] = bounds[k];
     // the benchmark-shaped fast path, or the fully general kernel
@@ -1331,11 +1388,55 @@ static cudaError_t launch_d(const AttnArgs& a, cudaStream_t stream) {
                    : launch_k<D, false, false>(tq, tk, tv, p, a.slices, stream);
 }
 
+// Head dims > 128 (the reference takes any d up to 133144, gemm.hpp:22,
+// attention.cpp:241-242): the general 16-warp kernel with S accumulated over
+// 128-column depth chunks of Q and K (exact int32 on the tensor core), one
+// launch per 128-column chunk of O (V and O offset to the chunk).  P depends on
+// S alone, so every launch makes the same codes; the audit is taken from the
+// first.
+static cudaError_t launch_wide(const AttnArgs& a, cudaStream_t stream) {
+    CUtensorMap tq, tk;
+    if (!make_map(&tq, a.q, a.slices, a.n, a.pitch, 128) ||
+        !make_map(&tk, a.k, a.slices, a.n, a.pitch, 128))
+        return cudaErrorInvalidValue;
+    Params p;
+    p.sq = a.sq;
+    p.sk = a.sk;
+    p.sv = a.sv;
+    p.n = static_cast<int32_t>(a.n);
+    p.d = static_cast<int32_t>(a.d);
+    p.bc = static_cast<int32_t>(a.bc < a.n ? a.bc : a.n);
+    p.flags = a.flags;
+    p.extra = (a.flags & IFA_FLAG_SQRT_D) ? 1.0f / sqrtf(static_cast<float>(a.d)) : 1.0f;
+    p.sk_mul = 1.4426950408889634f * p.extra;
+    p.q_tiles = static_cast<int32_t>((a.n + BM - 1) / BM);
+    p.slices = static_cast<int32_t>(a.slices);
+    p.items = p.q_tiles * p.slices;
+    p.wide_chunks = static_cast<int32_t>((a.d + 127) / 128);
+    p.o_pitch = a.d;
+    const float* bounds = code_bounds();
+    for (int k = 0; k < 128; ++k) p.bounds[k] = bounds[k];
+    const bool fast = (a.flags & IFA_FLAG_FAST) && a.audit == nullptr;
+    for (int64_t c0 = 0; c0 < a.d; c0 += 128) {
+        CUtensorMap tv;
+        if (!make_map(&tv, a.v + c0, a.slices, a.n, a.pitch, 128, a.pitch - c0))
+            return cudaErrorInvalidValue;
+        p.o = a.o + c0;
+        p.o_cols = static_cast<int32_t>(a.d - c0 < 128 ? a.d - c0 : 128);
+        p.audit = c0 == 0 ? a.audit : nullptr;
+        const cudaError_t e = fast ? launch_k<128, true, true>(tq, tk, tv, p, a.slices, stream)
+                                   : launch_k<128, true, false>(tq, tk, tv, p, a.slices, stream);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 }  // namespace attn
 
 cudaError_t launch_int_flash_fwd(const AttnArgs& a, cudaStream_t stream) {
     if (a.n > (int64_t{1} << 30) || ((a.n + 127) / 128) * a.slices > INT32_MAX)
         return cudaErrorInvalidValue;
+    if (a.d > 128) return attn::launch_wide(a, stream);
     if (int_flash_pp_eligible(a)) return launch_int_flash_pp(a, nullptr, stream);
     if (a.d <= 64) return attn::launch_d<64>(a, stream);
     return attn::launch_d<128>(a, stream);

@@ -112,6 +112,16 @@ constexpr int kPolyMask = IFA_PP_POLY_MASK;
 #define IFA_PP_MAGIC_CVT 0
 #endif
 constexpr bool kMagicCvt = IFA_PP_MAGIC_CVT != 0;
+// TMA epilogue variants (same-box A/B, attention ms, r2: per-half / per-box /
+// per-box + deferred read wait): C2 0.894 / 0.894 / 0.936, C3 1.963 / 1.960 /
+// 1.918, C5 55.53 / 55.12 / 57.64.  Deferring the last read wait to the next
+// item's first P store helps causal C3 and costs the non-causal lines.
+#ifndef IFA_PP_OBOX  // 1 = one bulk group per 32-column box, 0 = per 64-column half
+#define IFA_PP_OBOX 1
+#endif
+#ifndef IFA_PP_ODEFER  // 1 = the next item's first P stores wait for the O reads
+#define IFA_PP_ODEFER 0
+#endif
 #ifndef IFA_PP_EARLY_P
 #define IFA_PP_EARLY_P 1
 #endif
@@ -576,6 +586,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t sw = static_cast<uint32_t>(row0) & 7;  // same for row0 + 8
         Ring<KST> kv;
         uint32_t tc = 0, wi = 0;
+        // the previous item's O boxes (TMA epilogue) may still be reading the
+        // P buffer: the first P stores of the next item wait for them
+        bool o_pending = false;
+        const bool o_issuer = (mw & 7) == 0 && lane == 0;
+        auto o_reads_done = [&]() {
+            if (o_pending) {
+                if (o_issuer) tma_store_wait_read();
+                named_bar_sync(1 + g, 256);
+                o_pending = false;
+            }
+        };
 
         // group 1 starts ~1 us after group 0: started together, the two groups
         // run their MUFU-heavy and barrier-bound phases in lockstep on the same
@@ -744,6 +765,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     if constexpr (early_p) {
                         // P.V(j-1) has long finished by now: P is stored as it is made
                         if (tc > 0) bar_wait(bp_empty, (tc - 1) & 1);
+                        o_reads_done();
                         if (tr) PP_TR(0, g, tc, 3);
                         tc_fence_after();
                     }
@@ -852,6 +874,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     // P.V(j-1) done: the P buffer is free and O(j-1) is final
                     if constexpr (!early_p) {
                         if (tc > 0) bar_wait(bp_empty, (tc - 1) & 1);
+                        o_reads_done();
                         tc_fence_after();
                     }
                     if (tr) PP_TR(0, g, tc, 4);
@@ -931,6 +954,47 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 constexpr float os = MODE == kModeCodes ? 16777216.0f : 1.0f;
                 const uint32_t stage = smem_u32(sm.p[g]);
                 const bool issuer = (mw & 7) == 0 && lane == 0;
+if constexpr (IFA_PP_OBOX) {
+                // one bulk group per 128 x 32 box, boxes alternating between
+                // the two 16 KiB atoms: box c waits only for box c - 2's read
+#pragma unroll
+                for (int c = 0; c < D / 32; ++c) {
+                    if (c >= 2) {
+                        if (issuer) tma_store_wait_read_but1();
+                        named_bar_sync(1 + g, 256);
+                    }
+                    uint32_t o[16];
+                    ld16x256_x4(t_o + 32 * c, o);
+                    tmem_wait_ld();
+                    if (c == D / 32 - 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) bar_arrive(bo_free);
+                    }
+                    const uint32_t box = stage + (c & 1) * (BM * 128);
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        const uint32_t row = static_cast<uint32_t>(row0 + 8 * r);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint32_t q16 = (2 * k + (t0 >> 1)) ^ (row & 7);
+                            const float vx = __uint_as_float(o[4 * k + 2 * r]) * os * f[r];
+                            const float vy = __uint_as_float(o[4 * k + 2 * r + 1]) * os * f[r];
+                            asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(
+                                             box + row * 128 + q16 * 16 + (t0 & 1) * 8),
+                                         "f"(vx), "f"(vy)
+                                         : "memory");
+                        }
+                    }
+                    fence_proxy_async_shared();
+                    named_bar_sync(1 + g, 256);
+                    if (issuer) {
+                        tma_store_3d(&tm_o, reinterpret_cast<const uint8_t*>(sm.p[g]) + (c & 1) * (BM * 128),
+                                     32 * c, q0, slice);
+                        tma_store_commit();
+                    }
+                }
+} else {
 #pragma unroll
                 for (int hh = 0; hh < D / 64; ++hh) {
                     if (hh > 0) {  // the previous half's boxes have been read
@@ -973,9 +1037,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         tma_store_commit();
                     }
                 }
-                // the next item's P stores reuse the buffer
-                if (issuer) tma_store_wait_read();
-                named_bar_sync(1 + g, 256);
+}
+                if constexpr (IFA_PP_ODEFER) {
+                    o_pending = true;  // the next item's first P stores wait for these reads
+                } else {
+                    if (issuer) tma_store_wait_read();
+                    named_bar_sync(1 + g, 256);
+                }
                 if (tre) PP_TR(1, g, tc - 1, 7);
                 continue;
             }

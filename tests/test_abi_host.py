@@ -63,7 +63,11 @@ def test_abi_validation_mirrors_reference_exceptions():
     assert b"Br and Bc" in lib.ifa_last_error()
     assert _fwd(lib, d=133145) == _lib.IFA_EOVERFLOW   # gemm.cpp:22-28
     assert _fwd(lib, n=133145, bc=133145) == _lib.IFA_EOVERFLOW
-    assert _fwd(lib, d=129) == _lib.IFA_ENOTSUP
+    # head dims > 128 run (attn.cu launch_wide); the S / P-code dump does not
+    p = C.c_void_p(1)
+    assert lib.ifa_int_flash_fwd_dump(p, p, p, p, p, p, p, 1, 4, 129, 64, 128, _lib.FLAG_FAST,
+                                      p, None, None) == _lib.IFA_ENOTSUP
+    assert b"head dim 129" in lib.ifa_last_error()
     assert _fwd(lib, flags=8) == _lib.IFA_EINVAL
     assert _fwd(lib, slices=0) == _lib.IFA_OK          # nothing to do
     assert _fwd(lib, ptr=0) == _lib.IFA_EINVAL         # null pointers
