@@ -111,7 +111,8 @@ constexpr int kPolyMask = IFA_PP_POLY_MASK;
 #ifndef IFA_PP_MAGIC_CVT
 #define IFA_PP_MAGIC_CVT 0
 #endif
-constexpr bool kMagicCvt = IFA_PP_MAGIC_CVT != 0;
+// 0: I2F for every score, 1: magic add for every score, 2: for odd k, 3: for k % 4 == 3
+constexpr int kMagicCvt = IFA_PP_MAGIC_CVT;
 // TMA epilogue variants (same-box A/B, attention ms, r2: per-half / per-box /
 // per-box + deferred read wait): C2 0.894 / 0.894 / 0.936, C3 1.963 / 1.960 /
 // 1.918, C5 55.53 / 55.12 / 57.64.  Deferring the last read wait to the next
@@ -672,7 +673,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     if constexpr (MODE == kModeFp8) {
                         fa = make_float2(__uint_as_float(sr[4 * k]), __uint_as_float(sr[4 * k + 1]));
                         fb = make_float2(__uint_as_float(sr[4 * k + 2]), __uint_as_float(sr[4 * k + 3]));
-                    } else if constexpr (kMagicCvt) {
+                    } else if (kMagicCvt == 1 || (kMagicCvt == 2 && (k & 1)) ||
+                               (kMagicCvt == 3 && (k & 3) == 3)) {
                         // |S| <= 127^2 * 128 < 2^22: the bits of S + 0x4B400000 are
                         // the float 1.5 * 2^23 + S, so one exact packed subtract
                         // leaves float(S) (integer adds on the ALU instead of the

@@ -87,3 +87,70 @@ def test_wide_dump_is_refused(ifa):
     with pytest.raises(RuntimeError):
         ifa.int_flash_attention_dump(inputs, ifa.AttentionConfig(ifa.BlockSpec(64, 128),
                                                                  fast=True))
+
+
+# ---------------------------------------------------------------- every entry point
+def _p(a):
+    import ctypes as C
+    return C.c_void_p(a.ctypes.data)
+
+
+@pytest.mark.parametrize("n,d", [(256, 192), (130, 200)])
+def test_wide_host_entry_points(ifa, oracle, n, d):
+    """ifa_int_flash_fwd_host (codes in, exact, with audit) and
+    ifa_full_int8_attention_host (f32 in) at d > 128, bitwise vs the oracle."""
+    import ctypes as C
+    from paper_2409_16997_b200 import _lib
+    slices = 3
+    xs = [np.stack([oracle.slice_inputs("normal", n, d, seed=5 * s + 2)[r] for s in range(slices)])
+          for r in range(3)]
+    codes = []
+    for s in range(slices):
+        qc, qs = oracle.quantize_per_row(xs[0][s])
+        kc, ks = oracle.quantize_per_row(xs[1][s])
+        vc, vs = oracle.quantize_per_tensor(xs[2][s])
+        codes.append((qc, qs, kc, ks, vc, vs))
+    arr = [np.ascontiguousarray(np.stack([c[i] for c in codes])) for i in range(5)]
+    sv = np.array([c[5] for c in codes], np.float32)
+    lib = _lib.load()
+    o = np.zeros((slices, n, d), np.float32)
+    au = _lib.PCodeAuditC()
+    _lib.check(lib.ifa_int_flash_fwd_host(*[_p(a) for a in arr], _p(sv), _p(o), slices, n, d,
+                                          64, 128, 0, C.byref(au), None))
+    o2 = np.zeros((slices, n, d), np.float32)
+    xs = [np.ascontiguousarray(x) for x in xs]
+    _lib.check(lib.ifa_full_int8_attention_host(_p(xs[0]), _p(xs[1]), _p(xs[2]), _p(o2), slices,
+                                                n, d, 64, 128, 0, None))
+    mins, maxs, rows = [], [], 0
+    for s, (qc, qs, kc, ks, vc, vs) in enumerate(codes):
+        want, a = oracle.int_flash_attention(qc, qs, kc, ks, vc, vs, 64, 128, audit=True)
+        assert np.array_equal(o[s].view(np.uint32), want.view(np.uint32)), s
+        assert np.array_equal(o2[s].view(np.uint32), want.view(np.uint32)), s
+        mins.append(a[0])
+        maxs.append(a[1])
+        rows += a[3]
+    assert (au.min_code, au.max_code, au.rows_audited) == (min(mins), max(maxs), rows)
+
+
+@pytest.mark.parametrize("fast", [False, True])
+def test_wide_attention_plan(ifa, oracle, fast):
+    """runtime.AttentionPlan (quantize + attention, CUDA-graph replay) at d = 192
+    equals the quantize + int_flash_attention API calls bit for bit."""
+    import torch
+    from paper_2409_16997_b200.runtime import AttentionPlan
+    slices, n, d = 3, 256, 192
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q, k, v = (torch.randn(slices, n, d, device="cuda", generator=g) for _ in range(3))
+    plan = AttentionPlan(slices, n, d, bc=128, fast=fast)
+    got = plan.forward(q, k, v).clone()
+    plan.check()
+    inputs = ifa.QuantizedAttentionInputs(ifa.quantize_per_row(q), ifa.quantize_per_row(k),
+                                          ifa.quantize_per_tensor(v))
+    want = ifa.int_flash_attention(inputs, ifa.AttentionConfig(ifa.BlockSpec(128, 128),
+                                                               fast=fast))
+    assert torch.equal(got.view(torch.int32), want.view(torch.int32))
+    plan.capture(q, k, v)
+    plan.out.zero_()
+    plan.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(plan.out.view(torch.int32), want.view(torch.int32))
