@@ -108,6 +108,9 @@ constexpr int kPolyMask = IFA_PP_POLY_MASK;
 #define IFA_PP_SPARSE_HOT 16
 #endif
 // float(S) by integer magic add + packed subtract instead of I2F
+#ifndef IFA_PP_SPLIT_SLOAD
+#define IFA_PP_SPLIT_SLOAD 0
+#endif
 #ifndef IFA_PP_MAGIC_CVT
 #define IFA_PP_MAGIC_CVT 0
 #endif
@@ -638,9 +641,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (tr) PP_TR(0, g, tc, 0);
                 tc_fence_after();
                 uint32_t sr[64];
+                // IFA_PP_SPLIT_SLOAD: the second half of S is loaded while the
+                // first half is converted (tcgen05.wait::ld waits for every load)
+                constexpr bool split_sload = IFA_PP_SPLIT_SLOAD && !DUMP;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) ld16x256_x4(t_s + 32 * c, &sr[16 * c]);
+                for (int c = 0; c < (split_sload ? 2 : 4); ++c) ld16x256_x4(t_s + 32 * c, &sr[16 * c]);
                 tmem_wait_ld();
+                if constexpr (split_sload) {
+#pragma unroll
+                    for (int c = 2; c < 4; ++c) ld16x256_x4(t_s + 32 * c, &sr[16 * c]);
+                }
                 if constexpr (DUMP) {  // sr[4k + 2r + e]: row row0 + 8r, key 8k + 2 t0 + e
                     if (p.s_dump != nullptr) {
 #pragma unroll
@@ -657,9 +667,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         }
                     }
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) bar_arrive(bs_empty);
+                if constexpr (!split_sload) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) bar_arrive(bs_empty);
+                }
                 if (tr) PP_TR(0, g, tc, 1);
                 bar_wait(b_k_full + 8 * st, kv.phase);
                 // u = float(S) * sK * log2(e); sr[4k + {0,1}] row0, [4k + {2,3}] row1,
@@ -668,6 +680,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const float* skc = sm.sk[st] + 2 * t0;
 #pragma unroll
                 for (int k = 0; k < 16; ++k) {
+                    if (split_sload && k == 8) {  // the second half of S is in registers
+                        tmem_wait_ld();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) bar_arrive(bs_empty);
+                    }
                     const float2 s2 = *reinterpret_cast<const float2*>(skc + 8 * k);
                     float2 fa, fb;  // S as f32: exact int32 (kind::i8) or f32 (kind::f8f6f4)
                     if constexpr (MODE == kModeFp8) {
