@@ -58,18 +58,36 @@ constexpr int KST = IFA_PP_KST;  // K tiles (+ K scales) in flight
 constexpr int VST = IFA_PP_VST;  // fp16 V tiles in flight
 constexpr int CTRL_WARPS = 4;
 constexpr int GROUP_WARPS = 8;
-constexpr int NUM_THREADS = 32 * (CTRL_WARPS + 2 * GROUP_WARPS);
+// IFA_PP_EPI: a fourth warpgroup (warps 20-23, one per TMEM lane quarter)
+// writes each item's O (TMEM -> x sV/l -> global), so the math warps go on
+// to the next item without an epilogue; the math warps then run with 104
+// registers instead of 112 (the pool is 768 x 80).  Measured slower on the
+// non-causal lines (C2 +6%, C5 +5%; C3 -3% with EPI = 2): one warpgroup
+// serves both groups in turn, so group 1's next P.V(0) waits for both
+// epilogues.  EPI = 2 needs o_pitch * 4 % 16 == 0 (A/B builds only).
+#ifndef IFA_PP_EPI
+#define IFA_PP_EPI 0
+#endif
+constexpr bool kEpi = IFA_PP_EPI != 0;
+constexpr bool kEpi2 = IFA_PP_EPI == 2;  // O through shared memory + TMA stores
+constexpr int EPI_WARPS = kEpi ? 4 : 0;
+constexpr int EPI_WARP0 = CTRL_WARPS + 2 * GROUP_WARPS;
+constexpr int NUM_THREADS = 32 * (CTRL_WARPS + 2 * GROUP_WARPS + EPI_WARPS);
+constexpr int kLaunchRegs = kEpi ? 80 : 96;  // 65536 / NUM_THREADS, rounded down to 8
 #ifndef IFA_PP_REGS_CONTROL
 #define IFA_PP_REGS_CONTROL 32
 #endif
 constexpr uint32_t kRegsControl = IFA_PP_REGS_CONTROL;
+constexpr uint32_t kRegsEpi = 32;
 // setmaxnreg moves registers inside the CTA pool allocated at launch (640 x 96
 // = 61440): 4*32*32 + 16*32*112 = 61440.
 #ifndef IFA_PP_REGS_MATH
-#define IFA_PP_REGS_MATH 112
+#define IFA_PP_REGS_MATH (IFA_PP_EPI ? 104 : 112)
 #endif
 constexpr uint32_t kRegsMath = IFA_PP_REGS_MATH;
-static_assert(4 * kRegsControl + 16 * kRegsMath <= 640 * 96 / 32, "setmaxnreg pool");
+static_assert(4 * kRegsControl + EPI_WARPS * kRegsEpi + 16 * kRegsMath <=
+                  NUM_THREADS / 32 * kLaunchRegs,
+              "setmaxnreg pool");
 constexpr uint32_t TMEM_COLS = 512;
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
 constexpr float kLog2_127 = 6.9886846867721655f;
@@ -140,6 +158,11 @@ struct alignas(1024) Smem {
     uint64_t q_full, q_empty;
     uint64_t k_full[KST], k_empty[KST], v_full[VST], v_empty[VST];
     uint64_t s_full[2], s_empty[2], p_full[2], p_empty[2], o_full[2], o_free[2];
+    uint64_t epi_ready[2];  // IFA_PP_EPI: the group's per-row O factors are in epi_f
+    float epi_f[2][BM];     // IFA_PP_EPI: sV / l (or the mode's factor) per row
+    // IFA_PP_EPI == 2: per epilogue warp, two 32-row x 16-column f32 staging
+    // boxes (SW64) for TMA stores
+    alignas(1024) uint8_t epi_stage[kEpi2 ? 4 : 1][2][32 * 64];
     uint32_t tmem_base;
 };
 
@@ -355,6 +378,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t b_s_full = smem_u32(&sm.s_full[0]), b_s_empty = smem_u32(&sm.s_empty[0]);
     const uint32_t b_p_full = smem_u32(&sm.p_full[0]), b_p_empty = smem_u32(&sm.p_empty[0]);
     const uint32_t b_o_full = smem_u32(&sm.o_full[0]), b_o_free = smem_u32(&sm.o_free[0]);
+    const uint32_t b_epi_ready = smem_u32(&sm.epi_ready[0]);
 
     if (threadIdx.x == 0) {
         if (smem_u32(smem_raw) & 1023) __trap();
@@ -366,7 +390,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_init(&sm.p_full[i], GROUP_WARPS);
             mbar_init(&sm.p_empty[i], 1);
             mbar_init(&sm.o_full[i], 1);
-            mbar_init(&sm.o_free[i], GROUP_WARPS);
+            mbar_init(&sm.o_free[i], kEpi ? EPI_WARPS : GROUP_WARPS);
+            mbar_init(&sm.epi_ready[i], GROUP_WARPS);
         }
         for (int i = 0; i < KST; ++i) {
             mbar_init(&sm.k_full[i], 32);
@@ -384,7 +409,103 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
 
-    if (warp < CTRL_WARPS) {
+    if (kEpi && warp >= EPI_WARP0) {
+        // ----------------------------------------------- epilogue warpgroup
+        // Per item and group: O (TMEM, f32) x the group's per-row factor ->
+        // global, one row per thread (32x32b loads: lane = row), 16 columns
+        // = four 16-byte stores per step.  The math warps only publish the
+        // factors (epi_f + epi_ready) and go on to the next item; the group's
+        // next P.V(0) waits for o_free as before.
+        regs_dealloc<kRegsEpi>();
+        const uint32_t quarter = warp & 3;
+        const int32_t row = static_cast<int32_t>(quarter * 32 + lane);
+        const bool vec4 = p.o_pitch % 4 == 0 && (reinterpret_cast<uintptr_t>(p.o) & 15) == 0;
+        uint32_t wi = 0;
+        for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x, ++wi) {
+            const PWork w = pwork(idx, p, causal, J);
+#pragma unroll 1
+            for (int g = 0; g < 2; ++g) {
+                bar_wait(b_o_full + 8 * g, wi & 1);
+                bar_wait(b_epi_ready + 8 * g, wi & 1);
+                tc_fence_after();
+                const float f = sm.epi_f[g][row];
+                const int32_t grow = w.pair * 2 * BM + g * BM + row;
+                const uint32_t t_o = tmem + ((quarter * 32) << 16) + 256 * g + 128;
+                float* orow = p.o + (static_cast<int64_t>(w.slice) * n + grow) * p.o_pitch;
+#pragma unroll 1
+                for (int c = 0; c < D / 16; ++c) {
+                    uint32_t o[16];
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+                        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                        : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]), "=r"(o[4]), "=r"(o[5]),
+                          "=r"(o[6]), "=r"(o[7]), "=r"(o[8]), "=r"(o[9]), "=r"(o[10]), "=r"(o[11]),
+                          "=r"(o[12]), "=r"(o[13]), "=r"(o[14]), "=r"(o[15])
+                        : "r"(t_o + 16 * c));
+                    tmem_wait_ld();
+                    if (c == D / 16 - 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) bar_arrive(b_o_free + 8 * g);
+                    }
+                    if constexpr (kEpi2) {
+                        // 16-byte chunk v of row r at chunk v ^ ((r >> 1) & 3) of
+                        // its 64-byte line (SWIZZLE_64B): conflict-free quarter warps
+                        const uint32_t buf = smem_u32(sm.epi_stage[quarter][c & 1]);
+                        if (c >= 2) {  // box c - 2 (same buffer) has been read
+                            if (lane == 0) tma_store_wait_read_but1();
+                            __syncwarp();
+                        }
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) {
+                            const uint32_t chunk = static_cast<uint32_t>(v) ^ ((lane >> 1) & 3);
+                            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                             buf + lane * 64 + chunk * 16),
+                                         "f"(__uint_as_float(o[4 * v]) * f),
+                                         "f"(__uint_as_float(o[4 * v + 1]) * f),
+                                         "f"(__uint_as_float(o[4 * v + 2]) * f),
+                                         "f"(__uint_as_float(o[4 * v + 3]) * f)
+                                         : "memory");
+                        }
+                        fence_proxy_async_shared();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_3d(&tm_o, sm.epi_stage[quarter][c & 1], 16 * c,
+                                         w.pair * 2 * BM + g * BM + static_cast<int32_t>(quarter) * 32,
+                                         w.slice);
+                            tma_store_commit();
+                        }
+                        continue;
+                    }
+                    if (grow < n) {
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) {
+                            const int col = 16 * c + 4 * v;
+                            const float4 x = make_float4(__uint_as_float(o[4 * v]) * f,
+                                                         __uint_as_float(o[4 * v + 1]) * f,
+                                                         __uint_as_float(o[4 * v + 2]) * f,
+                                                         __uint_as_float(o[4 * v + 3]) * f);
+                            if (vec4 && col + 3 < p.d) {
+                                __stcs(reinterpret_cast<float4*>(orow + col), x);
+                            } else {
+                                if (col < p.d) orow[col] = x.x;
+                                if (col + 1 < p.d) orow[col + 1] = x.y;
+                                if (col + 2 < p.d) orow[col + 2] = x.z;
+                                if (col + 3 < p.d) orow[col + 3] = x.w;
+                            }
+                        }
+                    }
+                }
+                if constexpr (kEpi2) {  // the next group's boxes reuse the buffers
+                    if (lane == 0) tma_store_wait_read();
+                    __syncwarp();
+                }
+            }
+        }
+        if constexpr (kEpi2) {
+            if (lane == 0) tma_store_wait_all();
+        }
+    } else if (warp < CTRL_WARPS) {
         regs_dealloc<kRegsControl>();
         if (warp == 0) {
             // ------------------------------------------------------- producer
@@ -960,6 +1081,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     // V = decode / sV; an all-zero V slice (sV = 0) gives O = 0
                     f[r] = p.sv[slice] == 0.0f ? 0.0f : __fdiv_rn(__fdiv_rn(1.0f, lt), p.sv[slice]);
             }
+            if constexpr (kEpi) {
+                // hand the factors to the epilogue warpgroup; it has read the
+                // previous item's (o_free), and by induction o_free is at most
+                // one phase behind here, so the parity wait is unambiguous
+                constexpr float os = MODE == kModeCodes ? 16777216.0f : 1.0f;
+                if (wi > 0) bar_wait(bo_free, (wi - 1) & 1);
+                if (t0 == 0) {
+                    sm.epi_f[g][row0] = f[0] * os;
+                    sm.epi_f[g][row0 + 8] = f[1] * os;
+                }
+                __syncwarp();
+                if (lane == 0) bar_arrive(b_epi_ready + 8 * g);
+                continue;
+            }
             const bool tre = (mw & 7) == 0 && lane == 0;
             if (tre) PP_TR(1, g, tc - 1, 5);
             bar_wait(bo_full, wi & 1);
@@ -1209,6 +1344,23 @@ static bool make_map_o(CUtensorMap* map, const float* base, int64_t slices, int6
                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// IFA_PP_EPI == 2: f32 O [slices][n][o_pitch], box {16 cols, 32 rows, 1}, SW64
+static bool make_map_o_epi(CUtensorMap* map, const float* base, int64_t slices, int64_t n,
+                           int64_t d, int64_t o_pitch) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc || (o_pitch * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0)
+        return false;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(n),
+                                static_cast<cuuint64_t>(slices)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(o_pitch) * 4,
+                                   static_cast<cuuint64_t>(o_pitch) * 4 * n};
+    const cuuint32_t box[3] = {16u, 32u, 1u};
+    const cuuint32_t estr[3] = {1u, 1u, 1u};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
+               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int D, int MODE>
 static cudaError_t run(const void* q, const void* k, const __half* v16, const Params& p_in,
                        int64_t pitch, bool causal, cudaStream_t stream) {
@@ -1219,11 +1371,13 @@ static cudaError_t run(const void* q, const void* k, const __half* v16, const Pa
         return cudaErrorInvalidValue;
     Params p = p_in;
     const char* no_tma = std::getenv("IFA_B200_NO_OTMA");
-    p.o_tma = (!(no_tma && no_tma[0] == '1') && p.s_dump == nullptr && p.p_dump == nullptr &&
+    p.o_tma = (!kEpi && !(no_tma && no_tma[0] == '1') && p.s_dump == nullptr && p.p_dump == nullptr &&
                make_map_o(&to, p.o, p.slices, p.n, p.d, p.o_pitch))
                   ? 1
                   : 0;
     if (!p.o_tma) to = tq;  // unused
+    if (kEpi2 && !make_map_o_epi(&to, p.o, p.slices, p.n, p.d, p.o_pitch))
+        return cudaErrorInvalidValue;
     const size_t smem = sizeof(Smem<D>) + 1024;
     cudaError_t e = smem_attr_once<int_flash_pp_kernel<D, false, MODE, false>>(smem);
     if (e == cudaSuccess && MODE == kModeCodes) {
