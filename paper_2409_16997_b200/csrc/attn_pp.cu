@@ -71,7 +71,7 @@ constexpr int GROUP_WARPS = 8;
 constexpr bool kEpi = IFA_PP_EPI != 0;
 constexpr bool kEpi2 = IFA_PP_EPI == 2;  // O through shared memory + TMA stores
 constexpr int EPI_WARPS = kEpi ? 4 : 0;
-constexpr int EPI_WARP0 = CTRL_WARPS + 2 * GROUP_WARPS;
+[[maybe_unused]] constexpr int EPI_WARP0 = CTRL_WARPS + 2 * GROUP_WARPS;
 constexpr int NUM_THREADS = 32 * (CTRL_WARPS + 2 * GROUP_WARPS + EPI_WARPS);
 constexpr int kLaunchRegs = kEpi ? 80 : 96;  // 65536 / NUM_THREADS, rounded down to 8
 #ifndef IFA_PP_REGS_CONTROL
@@ -158,11 +158,13 @@ struct alignas(1024) Smem {
     uint64_t q_full, q_empty;
     uint64_t k_full[KST], k_empty[KST], v_full[VST], v_empty[VST];
     uint64_t s_full[2], s_empty[2], p_full[2], p_empty[2], o_full[2], o_free[2];
-    uint64_t epi_ready[2];  // IFA_PP_EPI: the group's per-row O factors are in epi_f
-    float epi_f[2][BM];     // IFA_PP_EPI: sV / l (or the mode's factor) per row
+#if IFA_PP_EPI
+    uint64_t epi_ready[2];  // the group's per-row O factors are in epi_f
+    float epi_f[2][BM];     // sV / l (or the mode's factor) per row
     // IFA_PP_EPI == 2: per epilogue warp, two 32-row x 16-column f32 staging
     // boxes (SW64) for TMA stores
     alignas(1024) uint8_t epi_stage[kEpi2 ? 4 : 1][2][32 * 64];
+#endif
     uint32_t tmem_base;
 };
 
@@ -378,7 +380,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t b_s_full = smem_u32(&sm.s_full[0]), b_s_empty = smem_u32(&sm.s_empty[0]);
     const uint32_t b_p_full = smem_u32(&sm.p_full[0]), b_p_empty = smem_u32(&sm.p_empty[0]);
     const uint32_t b_o_full = smem_u32(&sm.o_full[0]), b_o_free = smem_u32(&sm.o_free[0]);
+#if IFA_PP_EPI
     const uint32_t b_epi_ready = smem_u32(&sm.epi_ready[0]);
+#endif
 
     if (threadIdx.x == 0) {
         if (smem_u32(smem_raw) & 1023) __trap();
@@ -391,7 +395,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_init(&sm.p_empty[i], 1);
             mbar_init(&sm.o_full[i], 1);
             mbar_init(&sm.o_free[i], kEpi ? EPI_WARPS : GROUP_WARPS);
+#if IFA_PP_EPI
             mbar_init(&sm.epi_ready[i], GROUP_WARPS);
+#endif
         }
         for (int i = 0; i < KST; ++i) {
             mbar_init(&sm.k_full[i], 32);
@@ -409,7 +415,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
 
-    if (kEpi && warp >= EPI_WARP0) {
+#if IFA_PP_EPI
+    if (warp >= EPI_WARP0) {
         // ----------------------------------------------- epilogue warpgroup
         // Per item and group: O (TMEM, f32) x the group's per-row factor ->
         // global, one row per thread (32x32b loads: lane = row), 16 columns
@@ -505,7 +512,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if constexpr (kEpi2) {
             if (lane == 0) tma_store_wait_all();
         }
-    } else if (warp < CTRL_WARPS) {
+    } else
+#endif
+    if (warp < CTRL_WARPS) {
         regs_dealloc<kRegsControl>();
         if (warp == 0) {
             // ------------------------------------------------------- producer
@@ -1081,7 +1090,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     // V = decode / sV; an all-zero V slice (sV = 0) gives O = 0
                     f[r] = p.sv[slice] == 0.0f ? 0.0f : __fdiv_rn(__fdiv_rn(1.0f, lt), p.sv[slice]);
             }
-            if constexpr (kEpi) {
+#if IFA_PP_EPI
+            {
                 // hand the factors to the epilogue warpgroup; it has read the
                 // previous item's (o_free), and by induction o_free is at most
                 // one phase behind here, so the parity wait is unambiguous
@@ -1095,6 +1105,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (lane == 0) bar_arrive(b_epi_ready + 8 * g);
                 continue;
             }
+#endif
             const bool tre = (mw & 7) == 0 && lane == 0;
             if (tre) PP_TR(1, g, tc - 1, 5);
             bar_wait(bo_full, wi & 1);
