@@ -242,6 +242,15 @@ struct Work {
 // Work item -> (Q tile, slice).  Non-causal: the Q tiles of one slice are
 // adjacent, so CTAs running together share K/V in L2.  Causal: diagonal
 // tiles have the most keys, so they go first (longest-processing-time order).
+// The CTA's wi-th work item: causal items (longest first) are dealt in
+// rounds of gridDim.x taken in alternating directions, so no CTA gets the
+// longest item of every round (as attn_pp.cu); otherwise the grid stride.
+__device__ __forceinline__ int32_t item_at(uint32_t wi, bool snake) {
+    const int32_t G = static_cast<int32_t>(gridDim.x), c = static_cast<int32_t>(blockIdx.x);
+    const int32_t r = static_cast<int32_t>(wi);
+    return r * G + ((snake && (r & 1)) ? G - 1 - c : c);
+}
+
 __device__ __forceinline__ Work work_of(int32_t idx, const Params& p, bool causal) {
     Work w;
     int32_t qt;
@@ -456,7 +465,8 @@ __device__ __forceinline__ void softmax_quad(Smem<D>& sm, const Params& p, uint3
     Ring<STAGES> kv;
     uint32_t i = 0, pi = 0, bi = 0;
 
-    for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x) {
+    uint32_t wn = 0;
+    for (int32_t idx = item_at(0, causal); idx < p.items; idx = item_at(++wn, causal)) {
         const Work w = work_of(idx, p, causal);
         int32_t grow[2];
         float sq[2];
@@ -758,7 +768,7 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
         }
         Ring<STAGES> kv;
         uint32_t i = 0, wi = 0, ci = 0;
-        for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x, ++wi) {
+        for (int32_t idx = item_at(wi, causal); idx < p.items; idx = item_at(++wi, causal)) {
             const Work w = work_of(idx, p, causal);
             const uint32_t qb = wi & 1;
             if (lane == 0 && !wide) {
@@ -862,7 +872,7 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
                 __syncwarp();
                 if (kind & K_END) ++bi;
             };
-            for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x, ++wi) {
+            for (int32_t idx = item_at(wi, causal); idx < p.items; idx = item_at(++wi, causal)) {
                 const Work w = work_of(idx, p, causal);
                 const uint32_t qb = wi & 1;
                 if (!wide) bar_wait(b_q_full + 8 * qb, (wi >> 1) & 1);
@@ -960,7 +970,8 @@ __global__ void __launch_bounds__(QUAD ? 32 * (SOFT_WARP0 + QUAD_WARPS) : NUM_TH
         Ring<STAGES> kv;
         uint32_t i = 0, pi = 0, bi = 0;
 
-        for (int32_t idx = blockIdx.x; idx < p.items; idx += gridDim.x) {
+        uint32_t wn = 0;
+        for (int32_t idx = item_at(0, causal); idx < p.items; idx = item_at(++wn, causal)) {
             const Work w = work_of(idx, p, causal);
             const int32_t grow = w.q0 + row;
             const bool row_ok = grow < n;
