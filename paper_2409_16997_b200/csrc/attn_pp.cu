@@ -747,23 +747,41 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // sub-partitions (measured 0.994 -> 0.983 ms at C2, C5 -0.5%; per-item
         // delays hurt)
         if (IFA_PP_G1_DELAY_NS > 0 && g == 1) __nanosleep(IFA_PP_G1_DELAY_NS);
+        // sQ of the item's rows and sV of its slice, loaded one item ahead so
+        // the global-load latency (~700 cycles each) is not paid at the item
+        // boundary (the streamed step loads them after its per-slice wait)
+        auto load_scales = [&](int32_t item, float (&q_s)[2], float& v_s) {
+            if (item >= p.items) return;
+            const PWork nw = pwork(item, p, causal, J);
+            const int32_t nq0 = nw.pair * 2 * BM + static_cast<int32_t>(g) * BM;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int32_t gr = nq0 + row0 + 8 * r;
+                if constexpr (MODE == kModeFp8)
+                    q_s[r] = 1.0f;  // the scales are in the per-key constant
+                else
+                    q_s[r] = gr < n ? p.sq[static_cast<int64_t>(nw.slice) * n + gr] : 0.0f;
+            }
+            v_s = MODE == kModeHalf ? 1.0f : p.sv[nw.slice];
+        };
+        float nsq[2] = {0.0f, 0.0f}, nsv = 0.0f;
+        if constexpr (!STREAMED) load_scales(item_at<causal>(wi), nsq, nsv);
         for (int32_t idx = item_at<causal>(wi); idx < p.items; idx = item_at<causal>(++wi)) {
             const PWork w = pwork(idx, p, causal, J);
             const int32_t jg = group_tiles(w, static_cast<int>(g), causal, J);
             const int32_t diag = causal ? 2 * w.pair + static_cast<int32_t>(g) : -1;
             const int32_t q0 = w.pair * 2 * BM + static_cast<int32_t>(g) * BM;
             const int32_t slice = w.slice;
-            if constexpr (STREAMED) wait_slice_ready(p, slice);  // sQ, sV of a streamed step
-            int32_t grow[2];
-            float sq[2];
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                grow[r] = q0 + row0 + 8 * r;
-                if constexpr (MODE == kModeFp8)
-                    sq[r] = 1.0f;  // the scales are in the per-key constant
-                else
-                    sq[r] = grow[r] < n ? p.sq[static_cast<int64_t>(slice) * n + grow[r]] : 0.0f;
+            if constexpr (STREAMED) {
+                wait_slice_ready(p, slice);  // sQ, sV of a streamed step
+                load_scales(idx, nsq, nsv);
             }
+            int32_t grow[2];
+            float sq[2] = {nsq[0], nsq[1]};
+            const float sv_item = nsv;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) grow[r] = q0 + row0 + 8 * r;
+            if constexpr (!STREAMED) load_scales(item_at<causal>(wi + 1), nsq, nsv);
             float l[2] = {0.0f, 0.0f}, m[2] = {-__int_as_float(0x7f800000), -__int_as_float(0x7f800000)};
 
             for (int32_t j = 0; j < w.jt; ++j) {
@@ -1093,12 +1111,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 lt += __shfl_xor_sync(0xffffffffu, lt, 1);
                 lt += __shfl_xor_sync(0xffffffffu, lt, 2);
                 if constexpr (MODE == kModeCodes)
-                    f[r] = __fdiv_rn(p.sv[slice], lt);
+                    f[r] = __fdiv_rn(sv_item, lt);
                 else if constexpr (MODE == kModeHalf)
                     f[r] = __fdiv_rn(1.0f, lt);  // finalize_softmax_state (attention.cpp:139-149)
                 else
                     // V = decode / sV; an all-zero V slice (sV = 0) gives O = 0
-                    f[r] = p.sv[slice] == 0.0f ? 0.0f : __fdiv_rn(__fdiv_rn(1.0f, lt), p.sv[slice]);
+                    f[r] = sv_item == 0.0f ? 0.0f : __fdiv_rn(__fdiv_rn(1.0f, lt), sv_item);
             }
 #if IFA_PP_EPI
             {
