@@ -141,6 +141,9 @@ constexpr int kMagicCvt = IFA_PP_MAGIC_CVT;
 #ifndef IFA_PP_OBOX  // 1 = one bulk group per 32-column box, 0 = per 64-column half
 #define IFA_PP_OBOX 1
 #endif
+#ifndef IFA_PP_OSTG  // 1 = O staged in smem, read back row-contiguously, 16-byte global stores
+#define IFA_PP_OSTG 0
+#endif
 #ifndef IFA_PP_ODEFER  // 1 = the next item's first P stores wait for the O reads
 #define IFA_PP_ODEFER 0
 #endif
@@ -1147,8 +1150,64 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 // epilogue, tools/pp_trace.py).  Rows past n are clipped by TMA.
                 constexpr float os = MODE == kModeCodes ? 16777216.0f : 1.0f;
                 const uint32_t stage = smem_u32(sm.p[g]);
-                const bool issuer = (mw & 7) == 0 && lane == 0;
-if constexpr (IFA_PP_OBOX) {
+                [[maybe_unused]] const bool issuer = (mw & 7) == 0 && lane == 0;
+if constexpr (IFA_PP_OSTG) {
+                // Stage 64 columns at a time in the P buffer (same swizzled
+                // boxes), then read them back row-contiguously and store with
+                // 16-byte global stores, 512 contiguous bytes per half-warp:
+                // no TMA store (its smem reads wait behind the producer's
+                // loads of the next item), so the buffer is free as soon as
+                // the group has read it back.
+#pragma unroll 1
+                for (int hh = 0; hh < D / 64; ++hh) {
+                    if (hh > 0) named_bar_sync(1 + g, 256);  // the previous half is read back
+#pragma unroll
+                    for (int cc = 0; cc < 2; ++cc) {
+                        const int c = 2 * hh + cc;
+                        uint32_t o[16];
+                        ld16x256_x4(t_o + 32 * c, o);
+                        tmem_wait_ld();
+                        if (c == D / 32 - 1) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) bar_arrive(bo_free);
+                        }
+                        const uint32_t box = stage + cc * (BM * 128);
+#pragma unroll
+                        for (int r = 0; r < 2; ++r) {
+                            const uint32_t row = static_cast<uint32_t>(row0 + 8 * r);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const uint32_t q16 = (2 * k + (t0 >> 1)) ^ (row & 7);
+                                const float vx = __uint_as_float(o[4 * k + 2 * r]) * os * f[r];
+                                const float vy = __uint_as_float(o[4 * k + 2 * r + 1]) * os * f[r];
+                                asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(
+                                                 box + row * 128 + q16 * 16 + (t0 & 1) * 8),
+                                             "f"(vx), "f"(vy)
+                                             : "memory");
+                            }
+                        }
+                    }
+                    named_bar_sync(1 + g, 256);  // the half is staged
+                    const uint32_t gw = mw & 7;  // rows [16 gw, 16 gw + 16) of the group
+                    const uint32_t col4 = lane & 15, cc = col4 >> 3, q = col4 & 7;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const uint32_t row = 16 * gw + 2 * i + (lane >> 4);
+                        float4 x;
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                                     : "r"(stage + cc * (BM * 128) + row * 128 + ((q ^ (row & 7)) * 16)));
+                        const int32_t gr = q0 + static_cast<int32_t>(row);
+                        const int32_t col = 64 * hh + 4 * static_cast<int32_t>(col4);
+                        if (gr < n && col < p.d)
+                            __stcs(reinterpret_cast<float4*>(
+                                       p.o + (static_cast<int64_t>(slice) * n + gr) * p.o_pitch + col),
+                                   x);
+                    }
+                }
+                named_bar_sync(1 + g, 256);  // the next item's P stores reuse the buffer
+} else if constexpr (IFA_PP_OBOX) {
                 // one bulk group per 128 x 32 box, boxes alternating between
                 // the two 16 KiB atoms: box c waits only for box c - 2's read
 #pragma unroll
@@ -1232,7 +1291,8 @@ if constexpr (IFA_PP_OBOX) {
                     }
                 }
 }
-                if constexpr (IFA_PP_ODEFER) {
+                if constexpr (IFA_PP_OSTG) {
+                } else if constexpr (IFA_PP_ODEFER) {
                     o_pending = true;  // the next item's first P stores wait for these reads
                 } else {
                     if (issuer) tma_store_wait_read();
