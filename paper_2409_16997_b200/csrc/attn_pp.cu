@@ -132,7 +132,9 @@ constexpr int kPolyMask = IFA_PP_POLY_MASK;
 #ifndef IFA_PP_MAGIC_CVT
 #define IFA_PP_MAGIC_CVT 0
 #endif
-// 0: I2F for every score, 1: magic add for every score, 2: for odd k, 3: for k % 4 == 3
+// 0: I2F for every score, 1: magic add for every score, 2: for odd k, 3: for k % 4 == 3;
+// 4 / 5 / 6: as 1 / 2 / 3 but the magic add is an IMAD by an opaque 1 (the
+// FMA pipe's integer multiply-add instead of the ALU's IADD3)
 constexpr int kMagicCvt = IFA_PP_MAGIC_CVT;
 // TMA epilogue variants (same-box A/B, attention ms, r2: per-half / per-box /
 // per-box + deferred read wait): C2 0.894 / 0.894 / 0.936, C3 1.963 / 1.960 /
@@ -149,6 +151,13 @@ constexpr int kMagicCvt = IFA_PP_MAGIC_CVT;
 #endif
 #ifndef IFA_PP_EARLY_P
 #define IFA_PP_EARLY_P 1
+#endif
+// 1: the MMA issuers rebuild the Q / P descriptors at each issue (an opaque
+// register copy of the base the compiler cannot hoist), so the 32-register
+// control warps do not keep the eight P.V descriptors live across the loop
+// and spill them (reloaded between the P-full wait and the first P.V MMA)
+#ifndef IFA_PP_LAUNDER
+#define IFA_PP_LAUNDER 1
 #endif
 
 template <int D>
@@ -616,12 +625,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const uint32_t d_s = tmem + 256 * g, d_o = d_s + 128;
                 // descriptor + (byte offset >> 4) addresses the same layout at an
                 // offset (shared memory < 256 KiB: no carry out of the 14-bit field)
-                const uint64_t q_desc = smem_desc(smem_u32(sm.q[g]), 16, kSbo, kLayout);
-                const uint64_t p_desc = smem_desc(smem_u32(sm.p[g]), 16, 1024, kLayoutSw128);
+                const uint64_t q_desc_base = smem_desc(smem_u32(sm.q[g]), 16, kSbo, kLayout);
+                const uint64_t p_desc_base = smem_desc(smem_u32(sm.p[g]), 16, 1024, kLayoutSw128);
+                auto launder = [](uint64_t x) {
+                    if constexpr (IFA_PP_LAUNDER) asm volatile("mov.b64 %0, %0;" : "+l"(x));
+                    return x;
+                };
                 auto issue_s = [&](uint32_t ks, uint32_t kph) {
                     bar_wait(b_k_full + 8 * ks, kph);
                     tc_fence_after();
                     const uint64_t k_desc = smem_desc(smem_u32(sm.k[ks]), 16, kSbo, kLayout);
+                    const uint64_t q_desc = launder(q_desc_base);
                     if (elect_one()) {
 #pragma unroll
                         for (int kk = 0; kk < D / 32; ++kk) {
@@ -681,6 +695,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         if (lane == 0) PP_TR(1, g, t, 1);
                         if (j == 0 && wi > 0) bar_wait(b_o_free + 8 * g, (wi - 1) & 1);
                         tc_fence_after();
+                        const uint64_t p_desc = launder(p_desc_base);
                         if (elect_one()) {
 #pragma unroll
                             for (int kk = 0; kk < BN / 16; ++kk)
@@ -839,6 +854,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 // keys 8k + 2*t0 + {0,1}
                 float u[64];
                 const float* skc = sm.sk[st] + 2 * t0;
+                [[maybe_unused]] uint32_t one = 1u;
+                if constexpr (kMagicCvt >= 4) asm volatile("mov.b32 %0, %0;" : "+r"(one));
 #pragma unroll
                 for (int k = 0; k < 16; ++k) {
                     if (split_sload && k == 8) {  // the second half of S is in registers
@@ -852,6 +869,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     if constexpr (MODE == kModeFp8) {
                         fa = make_float2(__uint_as_float(sr[4 * k]), __uint_as_float(sr[4 * k + 1]));
                         fb = make_float2(__uint_as_float(sr[4 * k + 2]), __uint_as_float(sr[4 * k + 3]));
+                    } else if (kMagicCvt >= 4 && (kMagicCvt == 4 || (kMagicCvt == 5 && (k & 1)) ||
+                                                  (kMagicCvt == 6 && (k & 3) == 3))) {
+                        uint32_t x[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(x[e])
+                                : "r"(sr[4 * k + e]), "r"(one), "r"(0x4B400000u));
+                        fa = fsub2(make_float2(__uint_as_float(x[0]), __uint_as_float(x[1])), f2(kMagic));
+                        fb = fsub2(make_float2(__uint_as_float(x[2]), __uint_as_float(x[3])), f2(kMagic));
                     } else if (kMagicCvt == 1 || (kMagicCvt == 2 && (k & 1)) ||
                                (kMagicCvt == 3 && (k & 3) == 3)) {
                         // |S| <= 127^2 * 128 < 2^22: the bits of S + 0x4B400000 are
