@@ -156,31 +156,6 @@ constexpr int kMagicCvt = IFA_PP_MAGIC_CVT;
 // register copy of the base the compiler cannot hoist), so the 32-register
 // control warps do not keep the eight P.V descriptors live across the loop
 // and spill them (reloaded between the P-full wait and the first P.V MMA)
-// IFA_PP_RESCALE_FIRST: the O rescale (alpha != 1) runs right after the
-// P.V(j-1) wait, before the code loop, instead of after it.
-// IFA_PP_HALF_PUB (needs RESCALE_FIRST): P is published in two 64-key halves
-// (one MMA K-atom each): P.V(j) starts on the first half while the group
-// still computes the second.
-#ifndef IFA_PP_RESCALE_FIRST
-#define IFA_PP_RESCALE_FIRST 0
-#endif
-#ifndef IFA_PP_HALF_PUB
-#define IFA_PP_HALF_PUB 0
-#endif
-static_assert(!IFA_PP_HALF_PUB || IFA_PP_RESCALE_FIRST, "IFA_PP_HALF_PUB needs IFA_PP_RESCALE_FIRST");
-static_assert(!IFA_PP_RESCALE_FIRST || IFA_PP_EARLY_P, "IFA_PP_RESCALE_FIRST needs IFA_PP_EARLY_P");
-// Independent accumulation chains for the tensor core: one M128 N128 MMA
-// chain into a single accumulator runs at ~83 (kind::i8 K32) / ~108
-// (kind::f16 K16) cycles per MMA, two interleaved chains at ~66
-// (tools/microbench/mma_rate.cu).  IFA_PP_S_SPLIT: S as two N = 64 key halves
-// (separate TMEM columns), MMAs alternating between them; IFA_PP_PV_SPLIT
-// (D = 128): P.V as two N = 64 column halves of O, alternating.
-#ifndef IFA_PP_S_SPLIT
-#define IFA_PP_S_SPLIT 0
-#endif
-#ifndef IFA_PP_PV_SPLIT
-#define IFA_PP_PV_SPLIT 0
-#endif
 #ifndef IFA_PP_LAUNDER
 #define IFA_PP_LAUNDER 1
 #endif
@@ -195,7 +170,6 @@ struct alignas(1024) Smem {
     uint64_t q_full, q_empty;
     uint64_t k_full[KST], k_empty[KST], v_full[VST], v_empty[VST];
     uint64_t s_full[2], s_empty[2], p_full[2], p_empty[2], o_full[2], o_free[2];
-    uint64_t p_half[2];  // IFA_PP_HALF_PUB: the first 64 keys of P are in place
 #if IFA_PP_EPI
     uint64_t epi_ready[2];  // the group's per-row O factors are in epi_f
     float epi_f[2][BM];     // sV / l (or the mode's factor) per row
@@ -359,19 +333,6 @@ __device__ __forceinline__ void st16x256_x4(uint32_t taddr, const uint32_t* r) {
         : "memory");
 }
 
-__device__ __forceinline__ void ld16x256_x2(uint32_t taddr, uint32_t* r) {
-    asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
-                   "=r"(r[6]), "=r"(r[7])
-                 : "r"(taddr));
-}
-__device__ __forceinline__ void st16x256_x2(uint32_t taddr, const uint32_t* r) {
-    asm volatile("tcgen05.st.sync.aligned.16x256b.x2.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
-                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
-                 "r"(r[7])
-                 : "memory");
-}
-
 // kind::f16 instruction descriptor: D=F32, A=B=F16, A K-major.
 __host__ __device__ constexpr uint32_t idesc_f16(uint32_t m, uint32_t n, bool b_mn_major) {
     return (1u << 4) | ((b_mn_major ? 1u : 0u) << 16) | ((n >> 3) << 17) | ((m >> 4) << 24);
@@ -424,21 +385,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                      ? ((1u << 4) | ((BN >> 3) << 17) | ((BM >> 4) << 24))
                                      : idesc_i8(BM, BN, false, false);
     constexpr uint32_t kIdescPV = idesc_f16(BM, D, true);
-    constexpr bool kSSplit = IFA_PP_S_SPLIT != 0;
-    constexpr bool kPvSplit = IFA_PP_PV_SPLIT != 0 && D == 128;
-    constexpr uint32_t kIdescSh = MODE == kModeFp8
-                                      ? ((1u << 4) | ((64u >> 3) << 17) | ((BM >> 4) << 24))
-                                      : idesc_i8(BM, 64, false, false);
-    constexpr uint32_t kIdescPVh = idesc_f16(BM, 64, true);
-    // one P.V K-step (16 keys): N = D, or two N = 64 halves of O
-    auto mma_pv = [&](uint32_t d_o, uint64_t a, uint64_t b, uint32_t acc) {
-        if constexpr (kPvSplit) {
-            mma_f16_ss(d_o, a, b, kIdescPVh, acc);
-            mma_f16_ss(d_o + 64, a, b + (BN * 128 / 16), kIdescPVh, acc);
-        } else {
-            mma_f16_ss(d_o, a, b, kIdescPV, acc);
-        }
-    };
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     Smem<D>& sm = *reinterpret_cast<Smem<D>*>(smem_raw);
@@ -455,7 +401,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t b_v_full = smem_u32(&sm.v_full[0]), b_v_empty = smem_u32(&sm.v_empty[0]);
     const uint32_t b_s_full = smem_u32(&sm.s_full[0]), b_s_empty = smem_u32(&sm.s_empty[0]);
     const uint32_t b_p_full = smem_u32(&sm.p_full[0]), b_p_empty = smem_u32(&sm.p_empty[0]);
-    [[maybe_unused]] const uint32_t b_p_half = smem_u32(&sm.p_half[0]);
     const uint32_t b_o_full = smem_u32(&sm.o_full[0]), b_o_free = smem_u32(&sm.o_free[0]);
 #if IFA_PP_EPI
     const uint32_t b_epi_ready = smem_u32(&sm.epi_ready[0]);
@@ -469,7 +414,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_init(&sm.s_full[i], 1);
             mbar_init(&sm.s_empty[i], GROUP_WARPS);
             mbar_init(&sm.p_full[i], GROUP_WARPS);
-            mbar_init(&sm.p_half[i], GROUP_WARPS);
             mbar_init(&sm.p_empty[i], 1);
             mbar_init(&sm.o_full[i], 1);
             mbar_init(&sm.o_free[i], kEpi ? EPI_WARPS : GROUP_WARPS);
@@ -695,22 +639,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     if (elect_one()) {
 #pragma unroll
                         for (int kk = 0; kk < D / 32; ++kk) {
-                            if constexpr (kSSplit) {
-#pragma unroll
-                                for (int h = 0; h < 2; ++h) {
-                                    const uint64_t kd = k_desc + 2 * kk + h * ((64 * D) >> 4);
-                                    if constexpr (MODE == kModeFp8)
-                                        mma_f8_ss(d_s + 64 * h, q_desc + 2 * kk, kd, kIdescSh, kk > 0 ? 1u : 0u);
-                                    else
-                                        mma_i8_ss(d_s + 64 * h, q_desc + 2 * kk, kd, kIdescSh, kk > 0 ? 1u : 0u);
-                                }
-                            } else if constexpr (MODE == kModeFp8) {
+                            if constexpr (MODE == kModeFp8)
                                 mma_f8_ss(d_s, q_desc + 2 * kk, k_desc + 2 * kk, kIdescS,
                                           kk > 0 ? 1u : 0u);
-                            } else {
+                            else
                                 mma_i8_ss(d_s, q_desc + 2 * kk, k_desc + 2 * kk, kIdescS,
                                           kk > 0 ? 1u : 0u);
-                            }
                         }
                         mma_commit_u32(b_s_full + 8 * g);
                     }
@@ -757,29 +691,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         bar_wait(b_v_full + 8 * vr.idx, vr.phase);
                         const uint64_t v_desc =
                             smem_desc(smem_u32(sm.v[vr.idx]), BN * 128, 1024, kLayoutSw128);
-                        if (j == 0 && wi > 0) bar_wait(b_o_free + 8 * g, (wi - 1) & 1);
-                        constexpr int kk_first = IFA_PP_HALF_PUB ? BN / 32 : 0;
-                        if constexpr (IFA_PP_HALF_PUB) {
-                            bar_wait(b_p_half + 8 * g, t & 1);
-                            tc_fence_after();
-                            const uint64_t p_desc = launder(p_desc_base);
-                            if (elect_one()) {
-#pragma unroll
-                                for (int kk = 0; kk < kk_first; ++kk)
-                                    mma_pv(d_o, p_desc + (kk & 3) * 2, v_desc + kk * (16 * 128 / 16),
-                                           (j == 0 && kk == 0) ? 0u : 1u);
-                            }
-                            __syncwarp();
-                        }
                         bar_wait(b_p_full + 8 * g, t & 1);
                         if (lane == 0) PP_TR(1, g, t, 1);
+                        if (j == 0 && wi > 0) bar_wait(b_o_free + 8 * g, (wi - 1) & 1);
                         tc_fence_after();
                         const uint64_t p_desc = launder(p_desc_base);
                         if (elect_one()) {
 #pragma unroll
-                            for (int kk = kk_first; kk < BN / 16; ++kk)
-                                mma_pv(d_o, p_desc + (kk >> 2) * (BM * 128 / 16) + (kk & 3) * 2,
-                                       v_desc + kk * (16 * 128 / 16), (j == 0 && kk == 0) ? 0u : 1u);
+                            for (int kk = 0; kk < BN / 16; ++kk)
+                                mma_f16_ss(d_o, p_desc + (kk >> 2) * (BM * 128 / 16) + (kk & 3) * 2,
+                                           v_desc + kk * (16 * 128 / 16), kIdescPV,
+                                           (j == 0 && kk == 0) ? 0u : 1u);
                             mma_commit_u32(b_p_empty + 8 * g);
                             if (last) mma_commit_u32(b_o_full + 8 * g);
                             mma_commit_u32(b_v_empty + 8 * vr.idx);
@@ -1047,55 +969,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                      : "memory");
                     };
                     constexpr bool early_p = IFA_PP_EARLY_P;
-                    // O(j-1) *= alpha in TMEM for the rows whose max moved (O(j-1)
-                    // is final: P.V(j-1) has completed)
-                    auto rescale_o = [&]() {
-                        const bool need = j > 0 && (alpha[0] != 1.0f || alpha[1] != 1.0f);
-                        // 16 columns per load when the code loop's scores are live
-                        constexpr int kc = IFA_PP_RESCALE_FIRST ? 2 : 4;
-                        if (__any_sync(0xffffffffu, need)) {
-#pragma unroll
-                            for (int c = 0; c < D / (8 * kc); ++c) {
-                                uint32_t o[4 * kc];
-                                if constexpr (kc == 2)
-                                    ld16x256_x2(t_o + 16 * c, o);
-                                else
-                                    ld16x256_x4(t_o + 32 * c, o);
-                                tmem_wait_ld();
-#pragma unroll
-                                for (int k = 0; k < kc; ++k)
-#pragma unroll
-                                    for (int r = 0; r < 2; ++r) {
-                                        const float2 v = fmul2(make_float2(__uint_as_float(o[4 * k + 2 * r]),
-                                                                           __uint_as_float(o[4 * k + 2 * r + 1])),
-                                                               f2(alpha[r]));
-                                        o[4 * k + 2 * r] = __float_as_uint(v.x);
-                                        o[4 * k + 2 * r + 1] = __float_as_uint(v.y);
-                                    }
-                                if constexpr (kc == 2)
-                                    st16x256_x2(t_o + 16 * c, o);
-                                else
-                                    st16x256_x4(t_o + 32 * c, o);
-                            }
-                            tmem_wait_st();
-                        }
-                    };
-                    // IFA_PP_HALF_PUB: the first 64 keys of P (K-atom 0) are stored
-                    auto publish_half = [&]() {
-                        if constexpr (IFA_PP_HALF_PUB) {
-                            fence_proxy_async_shared();
-                            tc_fence_before();
-                            __syncwarp();
-                            if (lane == 0) bar_arrive(b_p_half + 8 * g);
-                        }
-                    };
                     if constexpr (early_p) {
                         // P.V(j-1) has long finished by now: P is stored as it is made
                         if (tc > 0) bar_wait(bp_empty, (tc - 1) & 1);
                         o_reads_done();
                         if (tr) PP_TR(0, g, tc, 3);
                         tc_fence_after();
-                        if constexpr (IFA_PP_RESCALE_FIRST) rescale_o();
                     }
                     if constexpr (MODE == kModeCodes) {
                         // full-INT8: y + 1.5*2^23 has the code round(y) in its low
@@ -1146,7 +1025,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                 if (early_p && (k & 3) == 3) {
                                     store_p(0, k >> 2, wd);
                                     store_p(1, k >> 2, wd);
-                                    if (k == 7) publish_half();
                                 }
                             }
                         };
@@ -1195,7 +1073,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             if (early_p && (k & 3) == 3) {
                                 store_p(0, k >> 2, wd);
                                 store_p(1, k >> 2, wd);
-                                if (k == 7) publish_half();
                             }
                         }
 #pragma unroll
@@ -1208,7 +1085,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         tc_fence_after();
                     }
                     if (tr) PP_TR(0, g, tc, 4);
-                    if constexpr (!IFA_PP_RESCALE_FIRST) rescale_o();
+                    const bool need = j > 0 && (alpha[0] != 1.0f || alpha[1] != 1.0f);
+                    if (__any_sync(0xffffffffu, need)) {
+    #pragma unroll
+                        for (int c = 0; c < D / 32; ++c) {
+                            uint32_t o[16];
+                            ld16x256_x4(t_o + 32 * c, o);
+                            tmem_wait_ld();
+    #pragma unroll
+                            for (int k = 0; k < 4; ++k)
+    #pragma unroll
+                                for (int r = 0; r < 2; ++r) {
+                                    const float2 v = fmul2(make_float2(__uint_as_float(o[4 * k + 2 * r]),
+                                                                       __uint_as_float(o[4 * k + 2 * r + 1])),
+                                                           f2(alpha[r]));
+                                    o[4 * k + 2 * r] = __float_as_uint(v.x);
+                                    o[4 * k + 2 * r + 1] = __float_as_uint(v.y);
+                                }
+                            st16x256_x4(t_o + 32 * c, o);
+                        }
+                        tmem_wait_st();
+                    }
                     if constexpr (!early_p) {
 #pragma unroll
                         for (int r = 0; r < 2; ++r)
