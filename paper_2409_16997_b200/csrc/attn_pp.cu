@@ -70,10 +70,23 @@ constexpr int GROUP_WARPS = 8;
 #endif
 constexpr bool kEpi = IFA_PP_EPI != 0;
 constexpr bool kEpi2 = IFA_PP_EPI == 2;  // O through shared memory + TMA stores
-constexpr int EPI_WARPS = kEpi ? 4 : 0;
+// IFA_PP_CORR: a fourth warpgroup (warps 20-23, one per TMEM lane quarter)
+// rescales O by alpha for both groups (FA4's correction warpgroup), so the O
+// rescale leaves the math warps' chain: the math warps publish alpha per row
+// (smem + alpha_ready), the correction warps rescale once P.V(j-1) is done
+// and arrive o_ready, and the MMA issuer waits o_ready before P.V(j).
+#ifndef IFA_PP_CORR
+#define IFA_PP_CORR 0
+#endif
+#ifndef IFA_PP_CORR_COLS  // O columns per TMEM load of a correction warp (8 or 16)
+#define IFA_PP_CORR_COLS 16
+#endif
+constexpr bool kCorr = IFA_PP_CORR != 0;
+static_assert(!(kEpi && kCorr), "IFA_PP_EPI and IFA_PP_CORR share the fourth warpgroup");
+constexpr int EPI_WARPS = (kEpi || kCorr) ? 4 : 0;
 [[maybe_unused]] constexpr int EPI_WARP0 = CTRL_WARPS + 2 * GROUP_WARPS;
 constexpr int NUM_THREADS = 32 * (CTRL_WARPS + 2 * GROUP_WARPS + EPI_WARPS);
-constexpr int kLaunchRegs = kEpi ? 80 : 96;  // 65536 / NUM_THREADS, rounded down to 8
+constexpr int kLaunchRegs = (kEpi || kCorr) ? 80 : 96;  // 65536 / NUM_THREADS, rounded down to 8
 #ifndef IFA_PP_REGS_CONTROL
 #define IFA_PP_REGS_CONTROL 32
 #endif
@@ -82,7 +95,7 @@ constexpr uint32_t kRegsEpi = 32;
 // setmaxnreg moves registers inside the CTA pool allocated at launch (640 x 96
 // = 61440): 4*32*32 + 16*32*112 = 61440.
 #ifndef IFA_PP_REGS_MATH
-#define IFA_PP_REGS_MATH (IFA_PP_EPI ? 104 : 112)
+#define IFA_PP_REGS_MATH ((IFA_PP_EPI || IFA_PP_CORR) ? 104 : 112)
 #endif
 constexpr uint32_t kRegsMath = IFA_PP_REGS_MATH;
 static_assert(4 * kRegsControl + EPI_WARPS * kRegsEpi + 16 * kRegsMath <=
@@ -152,6 +165,7 @@ constexpr int kMagicCvt = IFA_PP_MAGIC_CVT;
 #ifndef IFA_PP_EARLY_P
 #define IFA_PP_EARLY_P 1
 #endif
+static_assert(!kCorr || IFA_PP_EARLY_P, "IFA_PP_CORR publishes alpha after the early P-buffer wait");
 // 1: the MMA issuers rebuild the Q / P descriptors at each issue (an opaque
 // register copy of the base the compiler cannot hoist), so the 32-register
 // control warps do not keep the eight P.V descriptors live across the loop
@@ -176,6 +190,11 @@ struct alignas(1024) Smem {
     // IFA_PP_EPI == 2: per epilogue warp, two 32-row x 16-column f32 staging
     // boxes (SW64) for TMA stores
     alignas(1024) uint8_t epi_stage[kEpi2 ? 4 : 1][2][32 * 64];
+#endif
+#if IFA_PP_CORR
+    float alpha[2][2][BM];     // [group][tile parity][row]
+    uint64_t alpha_ready[2];   // the group's alpha of its current tile are in place
+    uint64_t o_ready[2];       // O(j-1) rescaled: P.V(j) may accumulate
 #endif
     uint32_t tmem_base;
 };
@@ -420,6 +439,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #if IFA_PP_EPI
             mbar_init(&sm.epi_ready[i], GROUP_WARPS);
 #endif
+#if IFA_PP_CORR
+            mbar_init(&sm.alpha_ready[i], GROUP_WARPS);
+            mbar_init(&sm.o_ready[i], EPI_WARPS);
+#endif
         }
         for (int i = 0; i < KST; ++i) {
             mbar_init(&sm.k_full[i], 32);
@@ -533,6 +556,73 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if constexpr (kEpi2) {
             if (lane == 0) tma_store_wait_all();
+        }
+    } else
+#endif
+#if IFA_PP_CORR
+    if (warp >= EPI_WARP0) {
+        // ------------------------------------------------- correction warpgroup
+        // Thread = one row of its lane quarter (32x32b loads).  Serves the two
+        // groups in whichever order their alpha arrive (non-blocking polls);
+        // the math warps publish alpha(t) once P.V(t-1) has completed.
+        regs_dealloc<kRegsEpi>();
+        const uint32_t quarter = warp & 3;
+        const uint32_t row = quarter * 32 + lane;
+        uint32_t total[2] = {0u, 0u};
+        {
+            uint32_t wi = 0;
+            for (int32_t idx = item_at<causal>(wi); idx < p.items; idx = item_at<causal>(++wi)) {
+                const PWork w = pwork(idx, p, causal, J);
+                total[0] += static_cast<uint32_t>(group_tiles(w, 0, causal, J));
+                total[1] += static_cast<uint32_t>(group_tiles(w, 1, causal, J));
+            }
+        }
+        const uint32_t b_alpha = smem_u32(&sm.alpha_ready[0]), b_oready = smem_u32(&sm.o_ready[0]);
+        uint32_t tcg[2] = {0u, 0u};
+        while (tcg[0] < total[0] || tcg[1] < total[1]) {
+            bool did = false;
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {  // unrolled: tcg / total stay in registers
+                const uint32_t t = tcg[g];
+                if (t >= total[g]) continue;
+                int ready = 0;
+                if (lane == 0) ready = bar_try(b_alpha + 8 * g, t & 1);  // implies P.V(t-1) done
+                if (!__shfl_sync(0xffffffffu, ready, 0)) continue;
+                tc_fence_after();
+                const float a = sm.alpha[g][t & 1][row];
+                if (__any_sync(0xffffffffu, a != 1.0f)) {
+                    const uint32_t t_o = tmem + ((quarter * 32) << 16) + 256 * g + 128;
+#pragma unroll 1
+                    for (int c = 0; c < D / IFA_PP_CORR_COLS; ++c) {
+                        uint32_t o[IFA_PP_CORR_COLS];
+                        if constexpr (IFA_PP_CORR_COLS == 16) {
+                            tmem_ld16(t_o + 16 * c, o);
+                        } else {
+                            tmem_ld8(t_o + 8 * c, o);
+                        }
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < IFA_PP_CORR_COLS; e += 2) {
+                            const float2 v = fmul2(make_float2(__uint_as_float(o[e]), __uint_as_float(o[e + 1])),
+                                                   f2(a));
+                            o[e] = __float_as_uint(v.x);
+                            o[e + 1] = __float_as_uint(v.y);
+                        }
+                        if constexpr (IFA_PP_CORR_COLS == 16) {
+                            tmem_st16(t_o + 16 * c, o);
+                        } else {
+                            tmem_st8(t_o + 8 * c, o);
+                        }
+                    }
+                    tmem_wait_st();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) bar_arrive(b_oready + 8 * g);
+                tcg[g] = t + 1;
+                did = true;
+            }
+            if (!did) __nanosleep(32);
         }
     } else
 #endif
@@ -692,6 +782,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         const uint64_t v_desc =
                             smem_desc(smem_u32(sm.v[vr.idx]), BN * 128, 1024, kLayoutSw128);
                         bar_wait(b_p_full + 8 * g, t & 1);
+#if IFA_PP_CORR
+                        bar_wait(smem_u32(&sm.o_ready[g]), t & 1);  // O(j-1) rescaled
+#endif
                         if (lane == 0) PP_TR(1, g, t, 1);
                         if (j == 0 && wi > 0) bar_wait(b_o_free + 8 * g, (wi - 1) & 1);
                         tc_fence_after();
@@ -953,6 +1046,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         alpha[r] = (j == 0 || mnew == m[r]) ? 1.0f : ex2(sq[r] * (m[r] - mnew));
                         m[r] = mnew;
                     }
+
                     if (tr) PP_TR(0, g, tc, 2);
                     // weights: 6 of 8 exp2 on MUFU, 2 on the FMA pipe.
                     // wd[r][k] = keys (8k + 2t0, +1) of row r as fp16x2.
@@ -972,6 +1066,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     if constexpr (early_p) {
                         // P.V(j-1) has long finished by now: P is stored as it is made
                         if (tc > 0) bar_wait(bp_empty, (tc - 1) & 1);
+#if IFA_PP_CORR
+                        // alpha to the correction warps, after P.V(j-1) is done: so
+                        // alpha_ready(j) also says O(j-1) is final, and can never run
+                        // two phases ahead of the correction warps (P.V(j) waits for them)
+                        if (t0 == 0) {
+                            sm.alpha[g][tc & 1][row0] = alpha[0];
+                            sm.alpha[g][tc & 1][row0 + 8] = alpha[1];
+                        }
+                        __syncwarp();
+                        if (lane == 0) bar_arrive(smem_u32(&sm.alpha_ready[g]));
+#endif
                         o_reads_done();
                         if (tr) PP_TR(0, g, tc, 3);
                         tc_fence_after();
@@ -1085,7 +1190,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         tc_fence_after();
                     }
                     if (tr) PP_TR(0, g, tc, 4);
-                    const bool need = j > 0 && (alpha[0] != 1.0f || alpha[1] != 1.0f);
+                    const bool need = !kCorr && j > 0 && (alpha[0] != 1.0f || alpha[1] != 1.0f);
                     if (__any_sync(0xffffffffu, need)) {
     #pragma unroll
                         for (int c = 0; c < D / 32; ++c) {
