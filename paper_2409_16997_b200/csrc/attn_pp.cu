@@ -78,6 +78,9 @@ constexpr bool kEpi2 = IFA_PP_EPI == 2;  // O through shared memory + TMA stores
 #ifndef IFA_PP_CORR
 #define IFA_PP_CORR 0
 #endif
+#ifndef IFA_PP_CORR_SLEEP_NS  // back-off between polls of the correction warps
+#define IFA_PP_CORR_SLEEP_NS 32
+#endif
 #ifndef IFA_PP_CORR_COLS  // O columns per TMEM load of a correction warp (8 or 16)
 #define IFA_PP_CORR_COLS 16
 #endif
@@ -622,7 +625,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 tcg[g] = t + 1;
                 did = true;
             }
-            if (!did) __nanosleep(32);
+            if (!did) __nanosleep(IFA_PP_CORR_SLEEP_NS);  // a poll costs the math warps issue slots
         }
     } else
 #endif
